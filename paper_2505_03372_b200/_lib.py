@@ -1,0 +1,101 @@
+"""ctypes binding of libwt_b200.so (the C-ABI declared in include/wt_b200.h).
+
+There is no CPU fallback: if the shared library is missing or cannot be
+loaded, importing the package raises.  Build it with
+``python -c "import __graft_entry__ as g; g.build()"`` (or ``make`` in
+``paper_2505_03372_b200/csrc``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .errors import BuildError, DeviceError, SymbolError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("WT_B200_LIB", os.path.join(_HERE, "libwt_b200.so"))
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libwt_b200.so not found at {LIB_PATH}: the CUDA library is required "
+        "(no CPU fallback). Build it with `make -C paper_2505_03372_b200/csrc`.")
+
+lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+
+WT_OK, WT_ERR_CUDA, WT_ERR_ARG, WT_ERR_OOM, WT_ERR_SYMBOL, WT_ERR_NCCL, WT_ERR_BUILD = range(7)
+Q_ACCESS, Q_RANK, Q_SELECT = 0, 1, 2
+B_RANK1, B_RANK0, B_SELECT1, B_SELECT0, B_BIT = range(5)
+F_DEVICE_PTRS, F_SYMBOLS, F_ACCESS_IDS = 1, 2, 4
+(A_SYMBOLS, A_CODE_VALUES, A_CODE_LENS, A_CUM_HIST, A_LEVEL_SIZES, A_REGION_OFFS, A_WORDS,
+ A_L1, A_L2, A_ONES, A_ZEROS, A_NODE_STARTS, A_NODE_RANK0) = range(13)
+
+
+class Meta(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("sigma", C.c_uint32), ("levels", C.c_uint32),
+                ("symbol_width", C.c_uint32), ("l2_bits", C.c_uint32),
+                ("sample_rate", C.c_uint64), ("first_coded", C.c_uint32),
+                ("device", C.c_uint32), ("n_words", C.c_uint64), ("device_bytes", C.c_uint64)]
+
+
+class LevelMeta(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in
+                ("n_bits", "total_ones", "n_l1", "n_l2", "n_ones", "n_zeros", "n_nodes")]
+
+
+_vp, _u64, _u32, _i32, _f32p = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(C.c_float)
+
+_SIGS = {
+    "wt_last_error": ([], C.c_char_p),
+    "wt_last_error_index": ([], C.c_int64),
+    "wt_abi_version": ([], C.c_int),
+    "wt_device_count": ([C.POINTER(C.c_int)], C.c_int),
+    "wt_construct": ([_vp, _u64, _i32, _i32, _vp, _u32, _i32, _u32, _u64, _i32, _vp,
+                      C.POINTER(_vp), _f32p], C.c_int),
+    "wt_tree_from_arrays": ([C.POINTER(Meta), _vp, _vp, _vp, C.POINTER(LevelMeta), _vp, _vp,
+                             _vp, _vp, _i32, C.POINTER(_vp)], C.c_int),
+    "wt_tree_meta": ([_vp, C.POINTER(Meta)], C.c_int),
+    "wt_tree_level_meta": ([_vp, _u32, C.POINTER(LevelMeta)], C.c_int),
+    "wt_tree_get": ([_vp, _i32, _u32, _vp, _u64], C.c_int),
+    "wt_tree_build_profile": ([_vp, _f32p, _u32], C.c_int),
+    "wt_tree_destroy": ([_vp], C.c_int),
+    "wt_tree_query": ([_vp, _i32, _vp, _vp, _vp, _u64, _u64, _i32, _vp, C.POINTER(C.c_int64), _f32p], C.c_int),
+    "wt_tree_level_query": ([_vp, _u32, _i32, _vp, _vp, _u64], C.c_int),
+    "wt_nccl_unique_id": ([_vp], C.c_int),
+    "wt_tree_replicate": ([_vp, _vp, _i32, _i32, _i32, C.POINTER(_vp), _f32p], C.c_int),
+    "wt_bits_build": ([_vp, _u64, _i32, _u32, _u64, _i32, C.POINTER(_vp)], C.c_int),
+    "wt_bits_level_meta": ([_vp, C.POINTER(LevelMeta)], C.c_int),
+    "wt_bits_get": ([_vp, _i32, _vp, _u64], C.c_int),
+    "wt_bits_query": ([_vp, _i32, _vp, _vp, _u64, _i32], C.c_int),
+    "wt_bits_destroy": ([_vp], C.c_int),
+}
+EXPORTS = tuple(_SIGS)
+
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map a nonzero status to the reference's exception classes."""
+    if rc == WT_OK:
+        return
+    msg = lib.wt_last_error().decode(errors="replace")
+    if rc == WT_ERR_SYMBOL:
+        raise SymbolError(msg)
+    if rc == WT_ERR_BUILD:
+        raise BuildError(msg)
+    if rc == WT_ERR_OOM:
+        raise MemoryError(f"{what}: {msg}")
+    raise DeviceError(f"{what}: {msg} (status {rc})")
+
+
+def ptr(a: np.ndarray | None):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def current_device() -> int:
+    return int(os.environ.get("WT_DEVICE", "0"))

@@ -1,0 +1,1175 @@
+// wt_capi.cu -- the extern "C" boundary (include/wt_b200.h) and the native
+// host runtime around the kernels: O(sigma) planning (codes, level sizes,
+// region layout, node tables), device memory, streams, the chunked host
+// query pipeline and NCCL replication.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <dlfcn.h>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/wt_b200.h"
+#include "wt_common.cuh"
+#include "wt_kernels.h"
+
+using namespace wt;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+static thread_local int64_t g_err_index = -1;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define CU(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      return fail(e_ == cudaErrorMemoryAllocation ? WT_ERR_OOM : WT_ERR_CUDA,           \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                  \
+    }                                                                                   \
+  } while (0)
+#define TRY(call)            \
+  do {                       \
+    int s_ = (call);         \
+    if (s_ != WT_OK) return s_; \
+  } while (0)
+
+extern "C" const char* wt_last_error(void) { return g_err.c_str(); }
+extern "C" int64_t wt_last_error_index(void) { return g_err_index; }
+extern "C" int wt_abi_version(void) { return WT_ABI_VERSION; }
+extern "C" int wt_device_count(int* count) {
+  CU(cudaGetDeviceCount(count));
+  return WT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// device memory: stream-ordered pool, kept warm across builds
+// ---------------------------------------------------------------------------
+static std::once_flag g_pool_once[64];
+static int setup_device(int device) {
+  CU(cudaSetDevice(device));
+  if (device >= 0 && device < 64) {
+    std::call_once(g_pool_once[device], [device]() {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+    });
+  }
+  return WT_OK;
+}
+
+static int sm_count(int device) {
+  int v = 148;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  return v;
+}
+
+template <typename T>
+static int dalloc(T** p, size_t count, cudaStream_t st) {
+  size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  CU(cudaMallocAsync((void**)p, bytes, st));
+  return WT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// O(sigma) planning (host): the reference's alphabet.py / wtree.py shape logic
+// ---------------------------------------------------------------------------
+static inline uint32_t ceil_log2_u(uint64_t s) {
+  uint32_t L = 0;
+  while ((1ull << L) < s) ++L;
+  return L;
+}
+static inline uint64_t prev_pow_two_u(uint64_t x) {  // alphabet.py:28-32
+  if (x <= 2) return 1;
+  uint64_t p = 1;
+  while (p * 2 < x) p *= 2;
+  return p;
+}
+
+struct Plan {
+  uint32_t sigma = 0, L = 0, first_coded = 0;
+  std::vector<uint16_t> symbols, values;
+  std::vector<uint8_t> lens;
+  std::vector<int64_t> hist, cum, sizes, offsets;
+  uint64_t n_words = 0;
+  std::vector<NodeEnt> nodes;
+  std::vector<uint64_t> node_off;  // start of level l in `nodes`
+  std::vector<std::vector<int64_t>> node_starts, node_rank0;
+  int code_bytes = 1;
+};
+
+// Reduced-tree codes (alphabet.py:160-207): the left/right path of every leaf
+// of the shape in which node [a,b) splits at a + prev_pow_two(b-a)
+// (wtree.py:388-403), left-aligned in an L-bit field.
+static void plan_codes(Plan& P) {
+  const uint32_t s = P.sigma, L = P.L;
+  P.values.resize(s);
+  P.lens.assign(s, (uint8_t)L);
+  for (uint32_t i = 0; i < s; ++i) P.values[i] = (uint16_t)i;
+  if ((s & (s - 1)) == 0) {
+    P.first_coded = s;
+    return;
+  }
+  P.first_coded = (uint32_t)prev_pow_two_u(s);
+  struct Item { uint32_t a, b, depth, path; };
+  std::vector<Item> todo{{P.first_coded, s, 1, 1}};
+  while (!todo.empty()) {
+    Item it = todo.back();
+    todo.pop_back();
+    const uint32_t w = it.b - it.a;
+    if ((w & (w - 1)) == 0) {  // complete subtree: path + plain offsets
+      uint32_t k = 0;
+      while ((1u << k) < w) ++k;
+      for (uint32_t o = 0; o < w; ++o) {
+        P.values[it.a + o] = (uint16_t)((((uint32_t)it.path << k) + o) << (L - it.depth - k));
+        P.lens[it.a + o] = (uint8_t)(it.depth + k);
+      }
+      continue;
+    }
+    const uint32_t p = (uint32_t)prev_pow_two_u(w);
+    todo.push_back({it.a, it.a + p, it.depth + 1, it.path << 1});
+    todo.push_back({it.a + p, it.b, it.depth + 1, (it.path << 1) | 1});
+  }
+}
+
+// hist (per id) known: cum_hist, level sizes, region layout, node tables.
+static void plan_shape(Plan& P, uint32_t l2_bits) {
+  (void)l2_bits;
+  const uint32_t s = P.sigma, L = P.L;
+  P.cum.assign(s + 1, 0);
+  for (uint32_t i = 0; i < s; ++i) P.cum[i + 1] = P.cum[i] + P.hist[i];
+  P.sizes.assign(L, 0);
+  for (uint32_t i = 0; i < s; ++i)
+    for (uint32_t l = 0; l < P.lens[i]; ++l) P.sizes[l] += P.hist[i];
+  P.offsets.assign(L, 0);
+  uint64_t cursor = 0;
+  for (uint32_t l = 0; l < L; ++l) {
+    P.offsets[l] = (int64_t)cursor;
+    cursor = (cursor + (uint64_t)P.sizes[l] + kAlignBits - 1) / kAlignBits * kAlignBits;
+  }
+  P.n_words = L ? ((uint64_t)P.offsets[L - 1] + (uint64_t)P.sizes[L - 1] + 63) / 64 : 0;
+  // node tables, level by level (wtree.py:388-433); keys are code prefixes
+  P.node_off.assign(L + 1, 0);
+  for (uint32_t l = 0; l < L; ++l) P.node_off[l + 1] = P.node_off[l] + (1ull << l);
+  P.nodes.assign(P.node_off[L], NodeEnt{0, 0, {-1, -1}});
+  P.node_starts.assign(L, {});
+  P.node_rank0.assign(L, {});
+  std::vector<std::pair<uint32_t, uint32_t>> cur, nxt;
+  if (L) cur.push_back({0, s});
+  for (uint32_t l = 0; l < L; ++l) {
+    int64_t zeros_before = 0;
+    nxt.clear();
+    for (auto [a, b] : cur) {
+      const uint32_t p = (uint32_t)prev_pow_two_u(b - a);
+      const uint32_t key = (uint32_t)P.values[a] >> (L - l);
+      const int64_t S = P.cum[a];
+      const int64_t Z = P.cum[a + p] - P.cum[a];
+      NodeEnt& ne = P.nodes[P.node_off[l] + key];
+      ne.zero_base = S - zeros_before;
+      ne.one_base = Z + zeros_before;
+      ne.leaf[0] = p == 1 ? (int)a : -1;
+      ne.leaf[1] = (b - a - p) == 1 ? (int)(a + p) : -1;
+      P.node_starts[l].push_back(a);
+      P.node_rank0[l].push_back(zeros_before);
+      zeros_before += Z;
+      if (p >= 2) nxt.push_back({a, a + p});
+      if (b - a - p >= 2) nxt.push_back({a + p, b});
+    }
+    cur.swap(nxt);
+  }
+  P.code_bytes = L <= 8 ? 1 : 2;
+}
+
+// ---------------------------------------------------------------------------
+// the tree handle
+// ---------------------------------------------------------------------------
+struct LevelHost {
+  wt_level_meta meta;
+  u64* l1 = nullptr;
+  u16* l2 = nullptr;
+  u64* ones = nullptr;
+  u64* zeros = nullptr;
+};
+
+struct wt_tree {
+  int device = 0;
+  wt_meta meta{};
+  Plan plan;
+  std::vector<LevelHost> lv;
+  u64* words = nullptr;
+  NodeEnt* nodes = nullptr;
+  u32* id_code = nullptr;
+  i64* cum = nullptr;
+  u16* symbols = nullptr;
+  int* sym2id = nullptr;
+  u64* bad = nullptr;  // first invalid query index (device scalar)
+  TreeDev dev{};
+  int rate_log = -1;
+  cudaStream_t stream = nullptr;
+  // query staging (reused across calls)
+  void* qbuf[2] = {nullptr, nullptr};
+  size_t qbuf_bytes = 0;
+  cudaStream_t qstream[2] = {nullptr, nullptr};
+  std::mutex qmutex;
+  // build profile: [0] text upload + histogram + plan, [1 + l] level-l kernel (ms)
+  std::vector<float> build_ms;
+};
+
+static int rate_log_of(uint64_t rate) {
+  if (rate && (rate & (rate - 1)) == 0) {
+    int r = 0;
+    while ((1ull << r) < rate) ++r;
+    return r;
+  }
+  return -1;
+}
+
+static void fill_treedev(wt_tree* t) {
+  TreeDev& D = t->dev;
+  memset(&D, 0, sizeof(D));
+  const Plan& P = t->plan;
+  for (uint32_t l = 0; l < P.L; ++l) {
+    LevelDev& d = D.lv[l];
+    const LevelHost& h = t->lv[l];
+    d.words = t->words + (P.offsets[l] >> 6);
+    d.l1 = h.l1;
+    d.l2 = h.l2;
+    d.ones = h.ones;
+    d.zeros = h.zeros;
+    d.nodes = t->nodes + P.node_off[l];
+    d.n_bits = h.meta.n_bits;
+    d.total_ones = h.meta.total_ones;
+    d.n_ones = h.meta.n_ones;
+    d.n_zeros = h.meta.n_zeros;
+    d.n_l1 = h.meta.n_l1;
+    d.n_l2 = h.meta.n_l2;
+  }
+  D.id_code = t->id_code;
+  D.cum = t->cum;
+  D.symbols = t->symbols;
+  D.sym2id = t->sym2id;
+  D.n = t->meta.n;
+  D.L = P.L;
+  D.sigma = P.sigma;
+  uint32_t sh = 0;
+  while ((1u << sh) < t->meta.l2_bits) ++sh;
+  D.l2_shift = sh;
+  D.width = t->meta.symbol_width;
+  D.rate = t->meta.sample_rate;
+  t->rate_log = rate_log_of(t->meta.sample_rate);
+}
+
+// allocate the per-level directories and upload the O(sigma) tables
+static int alloc_tree(wt_tree* t, cudaStream_t st) {
+  const Plan& P = t->plan;
+  t->lv.assign(P.L, LevelHost{});
+  TRY(dalloc(&t->words, P.n_words, st));
+  for (uint32_t l = 0; l < P.L; ++l) {
+    LevelHost& h = t->lv[l];
+    const uint64_t m = (uint64_t)P.sizes[l];
+    h.meta.n_bits = m;
+    h.meta.n_l1 = (m + kL1Bits - 1) / kL1Bits;
+    h.meta.n_l2 = (m + t->meta.l2_bits - 1) / t->meta.l2_bits;
+    h.meta.n_nodes = P.node_starts[l].size();
+    TRY(dalloc(&h.l1, h.meta.n_l1, st));
+    TRY(dalloc(&h.l2, h.meta.n_l2, st));
+    TRY(dalloc(&h.ones, m / t->meta.sample_rate, st));
+    TRY(dalloc(&h.zeros, m / t->meta.sample_rate, st));
+  }
+  TRY(dalloc(&t->nodes, P.nodes.size(), st));
+  TRY(dalloc(&t->id_code, P.sigma, st));
+  TRY(dalloc(&t->cum, P.sigma + 1, st));
+  TRY(dalloc(&t->symbols, P.sigma, st));
+  TRY(dalloc(&t->sym2id, 65536, st));
+  TRY(dalloc(&t->bad, 1, st));
+  std::vector<int> s2i(65536, -1);
+  for (uint32_t i = 0; i < P.sigma; ++i) s2i[P.symbols[i]] = (int)i;
+  CU(cudaMemcpyAsync(t->sym2id, s2i.data(), 65536 * 4, cudaMemcpyHostToDevice, st));
+  std::vector<u32> idc(P.sigma);
+  for (uint32_t i = 0; i < P.sigma; ++i) idc[i] = P.values[i] | ((u32)P.lens[i] << 16);
+  if (!P.nodes.empty())
+    CU(cudaMemcpyAsync(t->nodes, P.nodes.data(), P.nodes.size() * sizeof(NodeEnt),
+                       cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(t->id_code, idc.data(), idc.size() * 4, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(t->cum, P.cum.data(), P.cum.size() * 8, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(t->symbols, P.symbols.data(), P.symbols.size() * 2, cudaMemcpyHostToDevice,
+                     st));
+  CU(cudaStreamSynchronize(st));  // host vectors above are temporaries
+  uint64_t bytes = P.n_words * 8 + P.nodes.size() * sizeof(NodeEnt) + P.sigma * 14 + 8;
+  for (auto& h : t->lv)
+    bytes += h.meta.n_l1 * 8 + h.meta.n_l2 * 2 + 2 * (h.meta.n_bits / t->meta.sample_rate) * 8;
+  t->meta.device_bytes = bytes;
+  return WT_OK;
+}
+
+static void free_tree_arrays(wt_tree* t) {
+  cudaSetDevice(t->device);
+  auto F = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  F(t->words);
+  for (auto& h : t->lv) {
+    F(h.l1);
+    F(h.l2);
+    F(h.ones);
+    F(h.zeros);
+  }
+  F(t->nodes);
+  F(t->id_code);
+  F(t->cum);
+  F(t->symbols);
+  F(t->sym2id);
+  F(t->bad);
+  F(t->qbuf[0]);
+  F(t->qbuf[1]);
+  for (auto& s : t->qstream)
+    if (s) cudaStreamDestroy(s);
+  if (t->stream) cudaStreamDestroy(t->stream);
+}
+
+static int check_params(uint32_t l2_bits, uint64_t rate) {
+  if (l2_bits < 64 || (l2_bits & (l2_bits - 1)) || l2_bits > (uint32_t)kL1Bits)
+    return fail(WT_ERR_ARG, "l2_bits must be a power of two in [64, 65536]");
+  if (rate < 1) return fail(WT_ERR_ARG, "sample_rate must be positive");
+  return WT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// construction
+// ---------------------------------------------------------------------------
+struct Scratch {
+  std::vector<void*> ptrs;
+  cudaStream_t st;
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <typename T>
+  int get(T** p, size_t count) {
+    int s = dalloc(p, count, st);
+    if (s == WT_OK) ptrs.push_back(*p);
+    return s;
+  }
+};
+
+extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int text_on_device,
+                            const uint16_t* alphabet, uint32_t alphabet_len, int symbol_width,
+                            uint32_t l2_bits, uint64_t sample_rate, int device, void* stream,
+                            wt_tree** out, float* ms_out) {
+  g_err_index = -1;
+  if (!out) return fail(WT_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (n == 0) return fail(WT_ERR_BUILD, "cannot build an index over an empty text");
+  if (sym_bytes != 1 && sym_bytes != 2) return fail(WT_ERR_ARG, "sym_bytes must be 1 or 2");
+  if (symbol_width != 1 && symbol_width != 2) return fail(WT_ERR_ARG, "symbol_width must be 1 or 2");
+  TRY(check_params(l2_bits, sample_rate));
+  if (alphabet && alphabet_len == 0) return fail(WT_ERR_BUILD, "declared alphabet is empty");
+  if (text_on_device && ((uintptr_t)text & 15))
+    return fail(WT_ERR_ARG, "device text must be 16-byte aligned");
+  TRY(setup_device(device));
+  wt_tree* t = new wt_tree();
+  t->device = device;
+  int rc = WT_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!st) {
+    if (cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete t;
+      return fail(WT_ERR_CUDA, "stream create failed");
+    }
+    st = t->stream;
+  }
+  auto body = [&]() -> int {
+    Scratch S{{}, st};
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    struct EvGuard { cudaEvent_t a, b; ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); } } eg{e0, e1};
+    CU(cudaEventRecord(e0, st));
+    const void* dtext = text;
+    if (!text_on_device) {
+      u8* p;
+      TRY(S.get(&p, n * sym_bytes));
+      CU(cudaMemcpyAsync(p, text, n * sym_bytes, cudaMemcpyHostToDevice, st));
+      dtext = p;
+    }
+    const int nb = sym_bytes == 1 ? 256 : 65536;
+    u64* dhist;
+    TRY(S.get(&dhist, nb));
+    CU(cudaMemsetAsync(dhist, 0, nb * 8, st));
+    CU(launch_histogram(dtext, n, sym_bytes, dhist, sm_count(device), st));
+    std::vector<uint64_t> hraw(nb);
+    CU(cudaMemcpyAsync(hraw.data(), dhist, nb * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+
+    Plan& P = t->plan;
+    if (alphabet) {
+      P.symbols.assign(alphabet, alphabet + alphabet_len);
+      // every present symbol must be declared (alphabet.py:76-84)
+      std::vector<u8> member(nb, 0);
+      bool ok = true;
+      for (uint32_t i = 0; i < alphabet_len; ++i)
+        if (alphabet[i] < nb) member[alphabet[i]] = 1;
+      for (int s = 0; s < nb; ++s)
+        if (hraw[s] && !member[s]) ok = false;
+      if (!ok) {
+        u8* dm;
+        u64* dbest;
+        TRY(S.get(&dm, nb));
+        TRY(S.get(&dbest, 1));
+        CU(cudaMemcpyAsync(dm, member.data(), nb, cudaMemcpyHostToDevice, st));
+        CU(cudaMemsetAsync(dbest, 0xff, 8, st));
+        CU(launch_first_outside(dtext, n, sym_bytes, dm, dbest, sm_count(device), st));
+        uint64_t best = 0;
+        CU(cudaMemcpyAsync(&best, dbest, 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        uint32_t bad_sym = 0;
+        CU(cudaMemcpy(&bad_sym, (const u8*)dtext + best * sym_bytes, sym_bytes,
+                      cudaMemcpyDeviceToHost));
+        g_err_index = (int64_t)best;
+        char buf[160];
+        snprintf(buf, sizeof buf, "symbol %u at position %llu is not in the alphabet", bad_sym,
+                 (unsigned long long)best);
+        return fail(WT_ERR_SYMBOL, buf);
+      }
+    } else {
+      for (int s = 0; s < nb; ++s)
+        if (hraw[s]) P.symbols.push_back((uint16_t)s);
+    }
+    P.sigma = (uint32_t)P.symbols.size();
+    if (P.sigma > 65536) return fail(WT_ERR_BUILD, "alphabet size exceeds 65536");
+    P.L = ceil_log2_u(P.sigma);
+    P.hist.assign(P.sigma, 0);
+    for (uint32_t i = 0; i < P.sigma; ++i)
+      if (P.symbols[i] < nb) P.hist[i] = (int64_t)hraw[P.symbols[i]];
+    plan_codes(P);
+    plan_shape(P, l2_bits);
+
+    t->meta.n = n;
+    t->meta.sigma = P.sigma;
+    t->meta.levels = P.L;
+    t->meta.symbol_width = (uint32_t)symbol_width;
+    t->meta.l2_bits = l2_bits;
+    t->meta.sample_rate = sample_rate;
+    t->meta.first_coded = P.first_coded;
+    t->meta.device = (uint32_t)device;
+    t->meta.n_words = P.n_words;
+    TRY(alloc_tree(t, st));
+
+    // raw symbol -> code LUT for level 0, unless the map is the identity
+    std::vector<u16> lut(nb, 0);
+    bool identity = true;
+    for (uint32_t i = 0; i < P.sigma; ++i) {
+      if (P.symbols[i] >= nb) continue;
+      lut[P.symbols[i]] = P.values[i];
+      if (P.hist[i] && P.values[i] != P.symbols[i]) identity = false;
+    }
+    if (P.code_bytes != sym_bytes) identity = false;
+    u16* dlut = nullptr;
+    if (!identity && P.L) {
+      TRY(S.get(&dlut, nb));
+      CU(cudaMemcpyAsync(dlut, lut.data(), nb * 2, cudaMemcpyHostToDevice, st));
+    }
+
+    // zero the alignment gaps between regions (regions themselves are fully written)
+    for (uint32_t l = 0; l < P.L; ++l) {
+      const uint64_t end_w = ((uint64_t)P.offsets[l] + (uint64_t)P.sizes[l] + 63) / 64;
+      const uint64_t next_w = l + 1 < P.L ? (uint64_t)P.offsets[l + 1] / 64 : P.n_words;
+      if (next_w > end_w) CU(cudaMemsetAsync(t->words + end_w, 0, (next_w - end_w) * 8, st));
+    }
+
+    uint64_t max_tiles = 1;
+    for (uint32_t l = 0; l < P.L; ++l)
+      max_tiles = std::max<uint64_t>(max_tiles, level_tiles((uint64_t)P.sizes[l]));
+    u64* status;
+    u32* agg;
+    u64* totals;
+    TRY(S.get(&status, max_tiles));
+    TRY(S.get(&agg, max_tiles + 1));  // [max_tiles] = ticket counter
+    TRY(S.get(&totals, std::max<uint32_t>(P.L, 1)));
+    CU(cudaMemsetAsync(totals, 0, std::max<uint32_t>(P.L, 1) * 8, st));
+    void* cur[2] = {nullptr, nullptr};
+    if (P.L >= 2) {
+      u8* p;
+      TRY(S.get(&p, (uint64_t)P.sizes[1] * P.code_bytes + 16));
+      cur[0] = p;
+    }
+    if (P.L >= 3) {
+      u8* p;
+      TRY(S.get(&p, (uint64_t)P.sizes[2] * P.code_bytes + 16));
+      cur[1] = p;
+    }
+    uint32_t l2_log = 0;
+    while ((1u << l2_log) < l2_bits) ++l2_log;
+    std::vector<cudaEvent_t> lev(P.L + 1);
+    for (auto& e : lev) CU(cudaEventCreate(&e));
+    struct EvVec { std::vector<cudaEvent_t>& v; ~EvVec() { for (auto e : v) cudaEventDestroy(e); } } evg{lev};
+    for (uint32_t l = 0; l < P.L; ++l) {
+      const uint64_t m = (uint64_t)P.sizes[l];
+      CU(cudaEventRecord(lev[l], st));
+      if (m == 0) continue;
+      const uint32_t tiles = level_tiles(m);
+      CU(cudaMemsetAsync(status, 0, (size_t)tiles * 8, st));
+      CU(cudaMemsetAsync(agg, 0, (size_t)(max_tiles + 1) * 4, st));
+      LevelParams lp{};
+      lp.in = l == 0 ? dtext : cur[(l - 1) & 1];
+      lp.out = l + 1 < P.L ? cur[l & 1] : nullptr;
+      lp.m = m;
+      lp.m_next = l + 1 < P.L ? (uint64_t)P.sizes[l + 1] : 0;
+      if (lp.out && lp.m_next == 0) lp.out = nullptr;
+      lp.words = t->words + (P.offsets[l] >> 6);
+      LevelHost& h = t->lv[l];
+      lp.l1 = h.l1;
+      lp.l2 = h.l2;
+      lp.ones = h.ones;
+      lp.zeros = h.zeros;
+      lp.ones_cap = m / sample_rate;
+      lp.zeros_cap = m / sample_rate;
+      lp.nodes = t->nodes + P.node_off[l];
+      lp.lut = l == 0 ? dlut : nullptr;
+      lp.status = status;
+      lp.agg = agg;
+      lp.counter = agg + max_tiles;
+      lp.total_out = totals + l;
+      lp.shift_bit = P.L - 1 - l;
+      lp.shift_key = P.L - l;
+      lp.l2_log = l2_log;
+      lp.rate_log = rate_log_of(sample_rate);
+      lp.rate = sample_rate;
+      const int in_bytes = l == 0 ? sym_bytes : P.code_bytes;
+      CU(launch_level(lp, in_bytes, P.code_bytes, l == 0 && dlut != nullptr, st));
+    }
+    if (P.L) CU(cudaEventRecord(lev[P.L], st));
+    CU(cudaEventRecord(e1, st));
+    std::vector<uint64_t> tot(std::max<uint32_t>(P.L, 1));
+    CU(cudaMemcpyAsync(tot.data(), totals, tot.size() * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (uint32_t l = 0; l < P.L; ++l) {
+      wt_level_meta& m = t->lv[l].meta;
+      m.total_ones = tot[l];
+      m.n_ones = tot[l] / sample_rate;
+      m.n_zeros = (m.n_bits - tot[l]) / sample_rate;
+    }
+    fill_treedev(t);
+    if (ms_out) CU(cudaEventElapsedTime(ms_out, e0, e1));
+    t->build_ms.assign(P.L + 1, 0.f);
+    if (P.L) {
+      CU(cudaEventElapsedTime(&t->build_ms[0], e0, lev[0]));
+      for (uint32_t l = 0; l < P.L; ++l)
+        CU(cudaEventElapsedTime(&t->build_ms[1 + l], lev[l], lev[l + 1]));
+    }
+    return WT_OK;
+  };
+  rc = body();
+  if (rc == WT_OK) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(WT_ERR_CUDA, std::string("build: ") + cudaGetErrorString(e));
+  }
+  if (rc != WT_OK) {
+    cudaStreamSynchronize(st);
+    free_tree_arrays(t);
+    delete t;
+    return rc;
+  }
+  *out = t;
+  return WT_OK;
+}
+
+extern "C" int wt_tree_from_arrays(const wt_meta* meta, const uint16_t* symbols,
+                                   const int64_t* cum_hist, const uint64_t* words,
+                                   const wt_level_meta* levels, const int64_t* l1_cat,
+                                   const uint16_t* l2_cat, const int64_t* ones_cat,
+                                   const int64_t* zeros_cat, int device, wt_tree** out) {
+  if (!meta || !out) return fail(WT_ERR_ARG, "NULL argument");
+  TRY(check_params(meta->l2_bits, meta->sample_rate));
+  if (meta->sigma < 1 || meta->sigma > 65536) return fail(WT_ERR_ARG, "bad sigma");
+  TRY(setup_device(device));
+  wt_tree* t = new wt_tree();
+  t->device = device;
+  if (cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete t;
+    return fail(WT_ERR_CUDA, "stream create failed");
+  }
+  cudaStream_t st = t->stream;
+  auto body = [&]() -> int {
+    Plan& P = t->plan;
+    P.sigma = meta->sigma;
+    P.L = ceil_log2_u(P.sigma);
+    if (P.L != meta->levels) return fail(WT_ERR_ARG, "levels do not match sigma");
+    P.symbols.assign(symbols, symbols + P.sigma);
+    P.hist.resize(P.sigma);
+    for (uint32_t i = 0; i < P.sigma; ++i) P.hist[i] = cum_hist[i + 1] - cum_hist[i];
+    plan_codes(P);
+    plan_shape(P, meta->l2_bits);
+    t->meta = *meta;
+    t->meta.levels = P.L;
+    t->meta.first_coded = P.first_coded;
+    t->meta.device = (uint32_t)device;
+    if (t->meta.n_words != P.n_words) return fail(WT_ERR_ARG, "word count mismatch");
+    TRY(alloc_tree(t, st));
+    CU(cudaMemcpyAsync(t->words, words, P.n_words * 8, cudaMemcpyHostToDevice, st));
+    uint64_t o1 = 0, o2 = 0, o3 = 0, o4 = 0;
+    for (uint32_t l = 0; l < P.L; ++l) {
+      LevelHost& h = t->lv[l];
+      const wt_level_meta& m = levels[l];
+      if (m.n_bits != h.meta.n_bits || m.n_l1 != h.meta.n_l1 || m.n_l2 != h.meta.n_l2)
+        return fail(WT_ERR_ARG, "level directory shape mismatch");
+      h.meta.total_ones = m.total_ones;
+      h.meta.n_ones = m.n_ones;
+      h.meta.n_zeros = m.n_zeros;
+      if (m.n_l1) CU(cudaMemcpyAsync(h.l1, l1_cat + o1, m.n_l1 * 8, cudaMemcpyHostToDevice, st));
+      if (m.n_l2) CU(cudaMemcpyAsync(h.l2, l2_cat + o2, m.n_l2 * 2, cudaMemcpyHostToDevice, st));
+      if (m.n_ones)
+        CU(cudaMemcpyAsync(h.ones, ones_cat + o3, m.n_ones * 8, cudaMemcpyHostToDevice, st));
+      if (m.n_zeros)
+        CU(cudaMemcpyAsync(h.zeros, zeros_cat + o4, m.n_zeros * 8, cudaMemcpyHostToDevice, st));
+      o1 += m.n_l1;
+      o2 += m.n_l2;
+      o3 += m.n_ones;
+      o4 += m.n_zeros;
+    }
+    CU(cudaStreamSynchronize(st));
+    fill_treedev(t);
+    return WT_OK;
+  };
+  int rc = body();
+  if (rc != WT_OK) {
+    cudaStreamSynchronize(st);
+    free_tree_arrays(t);
+    delete t;
+    return rc;
+  }
+  *out = t;
+  return WT_OK;
+}
+
+extern "C" int wt_tree_meta(const wt_tree* t, wt_meta* out) {
+  if (!t || !out) return fail(WT_ERR_ARG, "NULL argument");
+  *out = t->meta;
+  return WT_OK;
+}
+
+extern "C" int wt_tree_level_meta(const wt_tree* t, uint32_t level, wt_level_meta* out) {
+  if (!t || !out || level >= t->plan.L) return fail(WT_ERR_ARG, "bad level");
+  *out = t->lv[level].meta;
+  return WT_OK;
+}
+
+static int copy_out(void* dst, const void* src, uint64_t bytes, uint64_t cap, bool device) {
+  if (bytes > cap) return fail(WT_ERR_ARG, "destination too small");
+  if (!bytes) return WT_OK;
+  if (device)
+    CU(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+  else
+    memcpy(dst, src, bytes);
+  return WT_OK;
+}
+
+extern "C" int wt_tree_get(const wt_tree* t, int what, uint32_t level, void* dst, uint64_t cap) {
+  if (!t) return fail(WT_ERR_ARG, "NULL tree");
+  const Plan& P = t->plan;
+  CU(cudaSetDevice(t->device));
+  const bool per_level = what >= WT_A_L1;
+  if (per_level && level >= P.L) return fail(WT_ERR_ARG, "bad level");
+  switch (what) {
+    case WT_A_SYMBOLS: return copy_out(dst, P.symbols.data(), P.sigma * 2ull, cap, false);
+    case WT_A_CODE_VALUES: return copy_out(dst, P.values.data(), P.sigma * 2ull, cap, false);
+    case WT_A_CODE_LENS: return copy_out(dst, P.lens.data(), P.sigma, cap, false);
+    case WT_A_CUM_HIST: return copy_out(dst, P.cum.data(), (P.sigma + 1ull) * 8, cap, false);
+    case WT_A_LEVEL_SIZES: return copy_out(dst, P.sizes.data(), P.L * 8ull, cap, false);
+    case WT_A_REGION_OFFS: return copy_out(dst, P.offsets.data(), P.L * 8ull, cap, false);
+    case WT_A_WORDS: return copy_out(dst, t->words, P.n_words * 8, cap, true);
+    case WT_A_L1: return copy_out(dst, t->lv[level].l1, t->lv[level].meta.n_l1 * 8, cap, true);
+    case WT_A_L2: return copy_out(dst, t->lv[level].l2, t->lv[level].meta.n_l2 * 2, cap, true);
+    case WT_A_ONES: return copy_out(dst, t->lv[level].ones, t->lv[level].meta.n_ones * 8, cap, true);
+    case WT_A_ZEROS:
+      return copy_out(dst, t->lv[level].zeros, t->lv[level].meta.n_zeros * 8, cap, true);
+    case WT_A_NODE_STARTS:
+      return copy_out(dst, P.node_starts[level].data(), P.node_starts[level].size() * 8, cap, false);
+    case WT_A_NODE_RANK0:
+      return copy_out(dst, P.node_rank0[level].data(), P.node_rank0[level].size() * 8, cap, false);
+    default: return fail(WT_ERR_ARG, "unknown array selector");
+  }
+}
+
+extern "C" int wt_tree_build_profile(const wt_tree* t, float* ms, uint32_t cap) {
+  if (!t || !ms) return fail(WT_ERR_ARG, "NULL argument");
+  for (uint32_t i = 0; i < cap; ++i) ms[i] = i < t->build_ms.size() ? t->build_ms[i] : 0.f;
+  return WT_OK;
+}
+
+extern "C" int wt_tree_destroy(wt_tree* t) {
+  if (!t) return WT_OK;
+  free_tree_arrays(t);
+  delete t;
+  return WT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// queries
+// ---------------------------------------------------------------------------
+extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int64_t* args,
+                             void* out, uint64_t m, uint64_t chunk, int flags, void* stream,
+                             int64_t* bad_index, float* ms_out) {
+  if (!t) return fail(WT_ERR_ARG, "NULL tree");
+  if (kind < 0 || kind > 2) return fail(WT_ERR_ARG, "unknown query kind");
+  if (ms_out) *ms_out = 0.f;
+  if (bad_index) *bad_index = -1;
+  if (m == 0) return WT_OK;
+  if (!args || !out || (kind != WT_Q_ACCESS && !ids)) return fail(WT_ERR_ARG, "NULL buffer");
+  CU(cudaSetDevice(t->device));
+  const bool validate = (flags & WT_F_SYMBOLS) != 0;
+  const int out_kind = kind != WT_Q_ACCESS ? 8
+                       : (flags & WT_F_ACCESS_IDS) ? 8 : (int)t->dev.width;
+  const size_t out_elem = (size_t)out_kind;
+  std::lock_guard<std::mutex> lk(t->qmutex);
+  if (flags & WT_F_DEVICE_PTRS) {
+    cudaStream_t st = stream ? (cudaStream_t)stream : t->stream;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (validate) CU(cudaMemsetAsync(t->bad, 0xff, 8, st));
+    if (ms_out) {
+      CU(cudaEventCreate(&e0));
+      CU(cudaEventCreate(&e1));
+      CU(cudaEventRecord(e0, st));
+    }
+    CU(launch_query(t->dev, kind, out_kind, validate, (const i64*)ids, (const i64*)args, out, m,
+                    t->rate_log, 0, t->bad, st));
+    if (ms_out) CU(cudaEventRecord(e1, st));
+    if (validate && bad_index)
+      CU(cudaMemcpyAsync(bad_index, t->bad, 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (ms_out) {
+      CU(cudaEventElapsedTime(ms_out, e0, e1));
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    return WT_OK;
+  }
+  // host buffers: chunked, double-buffered over two streams (
+  // batch.py:152-239 keeps at most two chunks staged)
+  if (chunk == 0) chunk = 1ull << 22;
+  if (chunk > m) chunk = m;
+  const size_t need = chunk * (16 + out_elem) + 64;
+  for (int i = 0; i < 2; ++i) {
+    if (!t->qstream[i]) CU(cudaStreamCreateWithFlags(&t->qstream[i], cudaStreamNonBlocking));
+    if (t->qbuf_bytes < need && t->qbuf[i]) {
+      CU(cudaFree(t->qbuf[i]));
+      t->qbuf[i] = nullptr;
+    }
+    if (!t->qbuf[i]) CU(cudaMalloc(&t->qbuf[i], need));
+  }
+  t->qbuf_bytes = std::max(t->qbuf_bytes, need);
+  if (validate) CU(cudaMemset(t->bad, 0xff, 8));
+  cudaEvent_t ev[2][2];
+  for (auto& a : ev)
+    for (auto& e : a) CU(cudaEventCreate(&e));
+  float total_ms = 0.f;
+  int rc = WT_OK;
+  const uint64_t nchunks = (m + chunk - 1) / chunk;
+  for (uint64_t c = 0; c < nchunks && rc == WT_OK; ++c) {
+    const int s = (int)(c & 1);
+    cudaStream_t st = t->qstream[s];
+    if (c >= 2 && ms_out) {  // harvest the timing of the chunk that used this slot
+      float ms = 0;
+      if (cudaEventSynchronize(ev[s][1]) == cudaSuccess &&
+          cudaEventElapsedTime(&ms, ev[s][0], ev[s][1]) == cudaSuccess)
+        total_ms += ms;
+    }
+    const uint64_t a = c * chunk, cnt = std::min(chunk, m - a);
+    u8* base = (u8*)t->qbuf[s];
+    i64* d_ids = (i64*)base;
+    i64* d_args = (i64*)(base + chunk * 8);
+    u8* d_out = base + chunk * 16;
+    if (kind != WT_Q_ACCESS &&
+        cudaMemcpyAsync(d_ids, ids + a, cnt * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+      rc = fail(WT_ERR_CUDA, "H2D ids");
+    if (rc == WT_OK &&
+        cudaMemcpyAsync(d_args, args + a, cnt * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+      rc = fail(WT_ERR_CUDA, "H2D args");
+    if (rc != WT_OK) break;
+    cudaEventRecord(ev[s][0], st);
+    cudaError_t e = launch_query(t->dev, kind, out_kind, validate, d_ids, d_args, d_out, cnt,
+                                 t->rate_log, a, t->bad, st);
+    if (e != cudaSuccess) {
+      rc = fail(WT_ERR_CUDA, std::string("query kernel: ") + cudaGetErrorString(e));
+      break;
+    }
+    cudaEventRecord(ev[s][1], st);
+    if (cudaMemcpyAsync((u8*)out + a * out_elem, d_out, cnt * out_elem, cudaMemcpyDeviceToHost,
+                        st) != cudaSuccess)
+      rc = fail(WT_ERR_CUDA, "D2H out");
+  }
+  for (int s = 0; s < 2; ++s) {
+    cudaError_t e = cudaStreamSynchronize(t->qstream[s]);
+    if (e != cudaSuccess && rc == WT_OK) rc = fail(WT_ERR_CUDA, cudaGetErrorString(e));
+  }
+  if (ms_out && rc == WT_OK) {
+    for (uint64_t c = nchunks >= 2 ? nchunks - 2 : 0; c < nchunks; ++c) {
+      float ms = 0;
+      const int s = (int)(c & 1);
+      if (cudaEventElapsedTime(&ms, ev[s][0], ev[s][1]) == cudaSuccess) total_ms += ms;
+    }
+    *ms_out = total_ms;
+  }
+  for (auto& a : ev)
+    for (auto& e : a) cudaEventDestroy(e);
+  if (rc == WT_OK && validate && bad_index) {
+    cudaError_t e = cudaMemcpy(bad_index, t->bad, 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = fail(WT_ERR_CUDA, cudaGetErrorString(e));
+  }
+  return rc;
+}
+
+// per-level bit-vector queries on a built tree (RankSelectIndex methods of
+// tree.rs[l], rankselect.py:140-373); args / out are host int64 arrays
+extern "C" int wt_tree_level_query(wt_tree* t, uint32_t level, int kind, const int64_t* args,
+                                   int64_t* out, uint64_t m) {
+  if (!t || level >= t->plan.L) return fail(WT_ERR_ARG, "bad level");
+  if (kind < 0 || kind > 4) return fail(WT_ERR_ARG, "unknown bit query kind");
+  if (m == 0) return WT_OK;
+  CU(cudaSetDevice(t->device));
+  cudaStream_t st = t->stream ? t->stream : 0;
+  Scratch S{{}, st};
+  i64 *da, *dout;
+  TRY(S.get(&da, m));
+  TRY(S.get(&dout, m));
+  CU(cudaMemcpyAsync(da, args, m * 8, cudaMemcpyHostToDevice, st));
+  CU(launch_bits_query(t->dev.lv[level], t->dev.l2_shift, t->dev.rate, t->rate_log, kind, da, dout,
+                       m, st));
+  CU(cudaMemcpyAsync(out, dout, m * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return WT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL replication (dlopen'ed so single-GPU use has no NCCL dependency)
+// ---------------------------------------------------------------------------
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int (*nccl_get_uid_t)(ncclUniqueId*);
+typedef int (*nccl_init_rank_t)(ncclComm_t*, int, ncclUniqueId, int);
+typedef int (*nccl_bcast_t)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
+typedef int (*nccl_destroy_t)(ncclComm_t);
+typedef const char* (*nccl_errstr_t)(int);
+typedef int (*nccl_group_t)(void);
+
+struct NcclApi {
+  bool ok = false;
+  nccl_get_uid_t get_uid;
+  nccl_init_rank_t init_rank;
+  nccl_bcast_t bcast;
+  nccl_destroy_t destroy;
+  nccl_errstr_t errstr;
+  nccl_group_t group_start, group_end;
+};
+static NcclApi g_nccl;
+static std::once_flag g_nccl_once;
+static int nccl_load() {
+  std::call_once(g_nccl_once, []() {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    g_nccl.get_uid = (nccl_get_uid_t)dlsym(h, "ncclGetUniqueId");
+    g_nccl.init_rank = (nccl_init_rank_t)dlsym(h, "ncclCommInitRank");
+    g_nccl.bcast = (nccl_bcast_t)dlsym(h, "ncclBroadcast");
+    g_nccl.destroy = (nccl_destroy_t)dlsym(h, "ncclCommDestroy");
+    g_nccl.errstr = (nccl_errstr_t)dlsym(h, "ncclGetErrorString");
+    g_nccl.group_start = (nccl_group_t)dlsym(h, "ncclGroupStart");
+    g_nccl.group_end = (nccl_group_t)dlsym(h, "ncclGroupEnd");
+    g_nccl.ok = g_nccl.get_uid && g_nccl.init_rank && g_nccl.bcast && g_nccl.destroy &&
+                g_nccl.group_start && g_nccl.group_end;
+  });
+  if (!g_nccl.ok) return fail(WT_ERR_NCCL, "libnccl.so.2 not loadable");
+  return WT_OK;
+}
+#define NC(call)                                                                        \
+  do {                                                                                  \
+    int r_ = (call);                                                                    \
+    if (r_ != 0)                                                                        \
+      return fail(WT_ERR_NCCL, std::string(#call) + ": " +                              \
+                                   (g_nccl.errstr ? g_nccl.errstr(r_) : "nccl error")); \
+  } while (0)
+
+extern "C" int wt_nccl_unique_id(uint8_t id[128]) {
+  TRY(nccl_load());
+  ncclUniqueId u;
+  NC(g_nccl.get_uid(&u));
+  memcpy(id, u.internal, 128);
+  return WT_OK;
+}
+
+// Root: its tree; others: NULL.  Small O(sigma) + metadata travel in one
+// broadcast of a host-packed header; the words and directories are broadcast
+// in place (ncclBroadcast over NVLink / NVSwitch), then every rank holds a
+// complete device-resident replica.
+extern "C" int wt_tree_replicate(wt_tree* root_tree, const uint8_t id[128], int rank, int world,
+                                 int device, wt_tree** out, float* ms_out) {
+  if (!out) return fail(WT_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (rank == 0 && !root_tree) return fail(WT_ERR_ARG, "root needs its tree");
+  TRY(nccl_load());
+  TRY(setup_device(device));
+  cudaStream_t st;
+  CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  ncclUniqueId u;
+  memcpy(u.internal, id, 128);
+  ncclComm_t comm;
+  NC(g_nccl.init_rank(&comm, world, u, rank));
+  struct CommGuard { ncclComm_t c; cudaStream_t s; ~CommGuard() { g_nccl.destroy(c); cudaStreamDestroy(s); } } cg{comm, st};
+  // 1. header: meta + per-level meta + symbols + cum (device staging buffer)
+  const size_t hdr_fixed = sizeof(wt_meta) + 16 * sizeof(wt_level_meta);
+  std::vector<u8> hdr;
+  uint64_t hdr_bytes = 0;
+  if (rank == 0) {
+    const wt_tree* t = root_tree;
+    hdr.resize(hdr_fixed + t->plan.sigma * 2 + (t->plan.sigma + 1) * 8);
+    memcpy(hdr.data(), &t->meta, sizeof(wt_meta));
+    for (uint32_t l = 0; l < t->plan.L; ++l)
+      memcpy(hdr.data() + sizeof(wt_meta) + l * sizeof(wt_level_meta), &t->lv[l].meta,
+             sizeof(wt_level_meta));
+    memcpy(hdr.data() + hdr_fixed, t->plan.symbols.data(), t->plan.sigma * 2);
+    memcpy(hdr.data() + hdr_fixed + t->plan.sigma * 2, t->plan.cum.data(), (t->plan.sigma + 1) * 8);
+    hdr_bytes = hdr.size();
+  }
+  u64* dsz;
+  CU(cudaMalloc(&dsz, 8));
+  CU(cudaMemcpy(dsz, &hdr_bytes, 8, cudaMemcpyHostToDevice));
+  NC(g_nccl.bcast(dsz, dsz, 8, /*ncclUint8*/ 1, 0, comm, st));
+  CU(cudaMemcpyAsync(&hdr_bytes, dsz, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  cudaFree(dsz);
+  hdr.resize(hdr_bytes);
+  u8* dh;
+  CU(cudaMalloc(&dh, hdr_bytes));
+  if (rank == 0) CU(cudaMemcpy(dh, hdr.data(), hdr_bytes, cudaMemcpyHostToDevice));
+  NC(g_nccl.bcast(dh, dh, hdr_bytes, 1, 0, comm, st));
+  CU(cudaMemcpyAsync(hdr.data(), dh, hdr_bytes, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  cudaFree(dh);
+  // 2. receivers allocate an identically shaped tree
+  wt_tree* t = nullptr;
+  if (rank == 0) {
+    t = root_tree;
+  } else {
+    t = new wt_tree();
+    t->device = device;
+    if (cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete t;
+      return fail(WT_ERR_CUDA, "stream create failed");
+    }
+    memcpy(&t->meta, hdr.data(), sizeof(wt_meta));
+    t->meta.device = (uint32_t)device;
+    Plan& P = t->plan;
+    P.sigma = t->meta.sigma;
+    P.L = t->meta.levels;
+    P.symbols.resize(P.sigma);
+    memcpy(P.symbols.data(), hdr.data() + hdr_fixed, P.sigma * 2);
+    std::vector<int64_t> cum(P.sigma + 1);
+    memcpy(cum.data(), hdr.data() + hdr_fixed + P.sigma * 2, (P.sigma + 1) * 8);
+    P.hist.resize(P.sigma);
+    for (uint32_t i = 0; i < P.sigma; ++i) P.hist[i] = cum[i + 1] - cum[i];
+    plan_codes(P);
+    plan_shape(P, t->meta.l2_bits);
+    int rc = alloc_tree(t, st);
+    if (rc != WT_OK) {
+      free_tree_arrays(t);
+      delete t;
+      return rc;
+    }
+    for (uint32_t l = 0; l < P.L; ++l)
+      memcpy(&t->lv[l].meta, hdr.data() + sizeof(wt_meta) + l * sizeof(wt_level_meta),
+             sizeof(wt_level_meta));
+  }
+  // 3. bulk arrays, one grouped broadcast
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  CU(cudaEventRecord(e0, st));
+  NC(g_nccl.group_start());
+  NC(g_nccl.bcast(t->words, t->words, t->plan.n_words * 8, 1, 0, comm, st));
+  for (uint32_t l = 0; l < t->plan.L; ++l) {
+    LevelHost& h = t->lv[l];
+    if (h.meta.n_l1) NC(g_nccl.bcast(h.l1, h.l1, h.meta.n_l1 * 8, 1, 0, comm, st));
+    if (h.meta.n_l2) NC(g_nccl.bcast(h.l2, h.l2, h.meta.n_l2 * 2, 1, 0, comm, st));
+    if (h.meta.n_ones) NC(g_nccl.bcast(h.ones, h.ones, h.meta.n_ones * 8, 1, 0, comm, st));
+    if (h.meta.n_zeros) NC(g_nccl.bcast(h.zeros, h.zeros, h.meta.n_zeros * 8, 1, 0, comm, st));
+  }
+  NC(g_nccl.group_end());
+  CU(cudaEventRecord(e1, st));
+  CU(cudaStreamSynchronize(st));
+  if (ms_out) cudaEventElapsedTime(ms_out, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rank != 0) fill_treedev(t);
+  *out = rank == 0 ? nullptr : t;
+  return WT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// stand-alone bit vectors (rankselect.build_index over one region)
+// ---------------------------------------------------------------------------
+struct wt_bits {
+  int device = 0;
+  u64* words = nullptr;
+  LevelHost h;
+  uint32_t l2_bits = 512, l2_shift = 9;
+  uint64_t rate = 1;
+  int rate_log = 0;
+  cudaStream_t stream = nullptr;
+};
+
+static LevelDev bits_dev(const wt_bits* b) {
+  LevelDev d{};
+  d.words = b->words;
+  d.l1 = b->h.l1;
+  d.l2 = b->h.l2;
+  d.ones = b->h.ones;
+  d.zeros = b->h.zeros;
+  d.n_bits = b->h.meta.n_bits;
+  d.total_ones = b->h.meta.total_ones;
+  d.n_ones = b->h.meta.n_ones;
+  d.n_zeros = b->h.meta.n_zeros;
+  d.n_l1 = b->h.meta.n_l1;
+  d.n_l2 = b->h.meta.n_l2;
+  return d;
+}
+
+static void free_bits(wt_bits* b) {
+  cudaSetDevice(b->device);
+  for (void* p : {(void*)b->words, (void*)b->h.l1, (void*)b->h.l2, (void*)b->h.ones,
+                  (void*)b->h.zeros})
+    if (p) cudaFree(p);
+  if (b->stream) cudaStreamDestroy(b->stream);
+}
+
+extern "C" int wt_bits_build(const uint64_t* words, uint64_t n_bits, int words_on_device,
+                             uint32_t l2_bits, uint64_t sample_rate, int device, wt_bits** out) {
+  if (!out) return fail(WT_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  TRY(check_params(l2_bits, sample_rate));
+  TRY(setup_device(device));
+  wt_bits* b = new wt_bits();
+  b->device = device;
+  b->l2_bits = l2_bits;
+  while ((1u << b->l2_shift) < l2_bits) ++b->l2_shift;
+  while ((1u << b->l2_shift) > l2_bits) --b->l2_shift;
+  b->rate = sample_rate;
+  b->rate_log = rate_log_of(sample_rate);
+  auto body = [&]() -> int {
+    CU(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+    cudaStream_t st = b->stream;
+    const uint64_t nw = (n_bits + 63) / 64;
+    wt_level_meta& m = b->h.meta;
+    m.n_bits = n_bits;
+    m.n_l1 = (n_bits + kL1Bits - 1) / kL1Bits;
+    m.n_l2 = (n_bits + l2_bits - 1) / l2_bits;
+    TRY(dalloc(&b->words, nw + 1, st));
+    if (nw) CU(cudaMemcpyAsync(b->words, words, nw * 8,
+                               words_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    TRY(dalloc(&b->h.l1, m.n_l1, st));
+    TRY(dalloc(&b->h.l2, m.n_l2, st));
+    TRY(dalloc(&b->h.ones, n_bits / sample_rate, st));
+    TRY(dalloc(&b->h.zeros, n_bits / sample_rate, st));
+    Scratch S{{}, st};
+    const uint32_t tiles = bits_tiles(n_bits);
+    u64* status;
+    u32* agg;
+    u64* total;
+    TRY(S.get(&status, tiles));
+    TRY(S.get(&agg, 1));
+    TRY(S.get(&total, 1));
+    CU(cudaMemsetAsync(status, 0, std::max<uint32_t>(tiles, 1) * 8, st));
+    CU(cudaMemsetAsync(agg, 0, 4, st));
+    CU(cudaMemsetAsync(total, 0, 8, st));
+    BitsParams p{};
+    p.words = b->words;
+    p.n_bits = n_bits;
+    p.l1 = b->h.l1;
+    p.l2 = b->h.l2;
+    p.ones = b->h.ones;
+    p.zeros = b->h.zeros;
+    p.ones_cap = n_bits / sample_rate;
+    p.zeros_cap = n_bits / sample_rate;
+    p.status = status;
+    p.agg = agg;
+    p.counter = agg;
+    p.total_out = total;
+    p.l2_log = b->l2_shift;
+    p.rate_log = b->rate_log;
+    p.rate = sample_rate;
+    CU(launch_bits_directory(p, st));
+    uint64_t tot = 0;
+    CU(cudaMemcpyAsync(&tot, total, 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    m.total_ones = tot;
+    m.n_ones = tot / sample_rate;
+    m.n_zeros = (n_bits - tot) / sample_rate;
+    return WT_OK;
+  };
+  int rc = body();
+  if (rc != WT_OK) {
+    if (b->stream) cudaStreamSynchronize(b->stream);
+    free_bits(b);
+    delete b;
+    return rc;
+  }
+  *out = b;
+  return WT_OK;
+}
+
+extern "C" int wt_bits_level_meta(const wt_bits* b, wt_level_meta* out) {
+  if (!b || !out) return fail(WT_ERR_ARG, "NULL argument");
+  *out = b->h.meta;
+  return WT_OK;
+}
+
+extern "C" int wt_bits_get(const wt_bits* b, int what, void* dst, uint64_t cap) {
+  if (!b) return fail(WT_ERR_ARG, "NULL bits");
+  CU(cudaSetDevice(b->device));
+  const wt_level_meta& m = b->h.meta;
+  switch (what) {
+    case WT_A_WORDS: return copy_out(dst, b->words, (m.n_bits + 63) / 64 * 8, cap, true);
+    case WT_A_L1: return copy_out(dst, b->h.l1, m.n_l1 * 8, cap, true);
+    case WT_A_L2: return copy_out(dst, b->h.l2, m.n_l2 * 2, cap, true);
+    case WT_A_ONES: return copy_out(dst, b->h.ones, m.n_ones * 8, cap, true);
+    case WT_A_ZEROS: return copy_out(dst, b->h.zeros, m.n_zeros * 8, cap, true);
+    default: return fail(WT_ERR_ARG, "unknown array selector");
+  }
+}
+
+extern "C" int wt_bits_query(wt_bits* b, int kind, const int64_t* args, int64_t* out, uint64_t m,
+                             int flags) {
+  if (!b) return fail(WT_ERR_ARG, "NULL bits");
+  if (kind < 0 || kind > 4) return fail(WT_ERR_ARG, "unknown bit query kind");
+  if (m == 0) return WT_OK;
+  CU(cudaSetDevice(b->device));
+  cudaStream_t st = b->stream;
+  const LevelDev d = bits_dev(b);
+  if (flags & WT_F_DEVICE_PTRS) {
+    CU(launch_bits_query(d, b->l2_shift, b->rate, b->rate_log, kind, (const i64*)args, (i64*)out, m, st));
+    CU(cudaStreamSynchronize(st));
+    return WT_OK;
+  }
+  Scratch S{{}, st};
+  i64 *da, *dout;
+  TRY(S.get(&da, m));
+  TRY(S.get(&dout, m));
+  CU(cudaMemcpyAsync(da, args, m * 8, cudaMemcpyHostToDevice, st));
+  CU(launch_bits_query(d, b->l2_shift, b->rate, b->rate_log, kind, da, dout, m, st));
+  CU(cudaMemcpyAsync(out, dout, m * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return WT_OK;
+}
+
+extern "C" int wt_bits_destroy(wt_bits* b) {
+  if (!b) return WT_OK;
+  free_bits(b);
+  delete b;
+  return WT_OK;
+}

@@ -1,0 +1,71 @@
+// wt_kernels.h -- host-visible launch wrappers of the CUDA kernels.
+#pragma once
+#include "wt_common.cuh"
+
+namespace wt {
+
+// K2 parameters for one level (wt_level.cu)
+struct LevelParams {
+  const void* in;      // level input: text (level 0) or the partitioned codes
+  void* out;           // next level's codes (nullptr at the last level)
+  u64 m, m_next;       // level_sizes[l], level_sizes[l+1]
+  u64* words;          // region start
+  u64* l1;
+  u16* l2;
+  u64* ones;
+  u64* zeros;
+  u64 ones_cap, zeros_cap;
+  const NodeEnt* nodes;  // 2^l entries keyed by the l-bit code prefix
+  const u16* lut;        // level 0: raw symbol -> code (nullptr: identity)
+  u64* status;           // per tile look-back word
+  u32* agg;              // per tile aggregate + 1
+  u32* counter;          // dynamic tile ticket
+  u64* total_out;        // total ones of the level
+  u32 shift_bit;         // L-1-l
+  u32 shift_key;         // L-l
+  u32 l2_log;
+  int rate_log;          // log2(rate) when rate is a power of two, else -1
+  u64 rate;
+};
+
+cudaError_t launch_level(const LevelParams& p, int in_bytes, int code_bytes, bool lut,
+                         cudaStream_t st);
+u32 level_tiles(u64 m);
+
+// K1: raw-symbol histogram (wt_hist.cu); hist must be zeroed (u64[256|65536])
+cudaError_t launch_histogram(const void* text, u64 n, int sym_bytes, u64* hist, int sms,
+                             cudaStream_t st);
+// first text position whose raw symbol has member[sym] == 0; *best preset to ~0
+cudaError_t launch_first_outside(const void* text, u64 n, int sym_bytes, const u8* member,
+                                 u64* best, int sms, cudaStream_t st);
+
+// Q kernels (wt_query.cu)
+// kind 0/1/2 = access/rank/select; out_kind (access): 1|2 = symbol bytes, 8 = int64 id;
+// validate: ids are original symbols, invalid queries -> atomicMin(bad, base + i)
+cudaError_t launch_query(const TreeDev& T, int kind, int out_kind, bool validate, const i64* ids,
+                         const i64* args, void* out, u64 m, int rate_log, u64 base, u64* bad,
+                         cudaStream_t st);
+
+// single bit-vector index (wt_bits.cu)
+struct BitsParams {
+  const u64* words;
+  u64 n_bits;
+  u64* l1;
+  u16* l2;
+  u64* ones;
+  u64* zeros;
+  u64 ones_cap, zeros_cap;
+  u64* status;
+  u32* agg;
+  u32* counter;
+  u64* total_out;
+  u32 l2_log;
+  int rate_log;
+  u64 rate;
+};
+cudaError_t launch_bits_directory(const BitsParams& p, cudaStream_t st);
+u32 bits_tiles(u64 n_bits);
+cudaError_t launch_bits_query(const LevelDev& L, u32 l2_shift, u64 rate, int rate_log, int kind,
+                              const i64* args, i64* out, u64 m, cudaStream_t st);
+
+}  // namespace wt

@@ -1,0 +1,86 @@
+// wt_rs.cuh -- device rank / select over one level's directory.
+//
+// rank1: Alg. 1 (rankselect.py:151-169): L1[p>>16] + L2[p>>l2_shift] + popcount
+//        of the words between the L2 block start and p, masked last word;
+//        p == n_bits -> total_ones.
+// select: Alg. 2 (rankselect.py:229-367): sample window -> binary search over
+//        L1 -> binary search over L2 -> word scan -> in-word select (here one
+//        __fns instead of the popcount halving; the k-th set bit is unique so
+//        the answer is identical).
+#pragma once
+#include "wt_common.cuh"
+
+namespace wt {
+
+__device__ __forceinline__ u64 rank1_dev(const LevelDev& L, u64 p, u32 l2_shift) {
+  if (p >= L.n_bits) return L.total_ones;
+  u64 r = __ldg(L.l1 + (p >> 16)) + (u64)__ldg(L.l2 + (p >> l2_shift));
+  const u64 wb = (p >> l2_shift) << (l2_shift - 6);
+  const u64 we = p >> 6;
+  for (u64 w = wb; w < we; ++w) r += __popcll(__ldg(L.words + w));
+  const u32 rem = (u32)(p & 63);
+  if (rem) r += __popcll(__ldg(L.words + we) & ((1ull << rem) - 1));
+  return r;
+}
+
+// rank1 when the word holding p is already loaded (p < n_bits)
+__device__ __forceinline__ u64 rank1_with_word(const LevelDev& L, u64 p, u32 l2_shift, u64 wp) {
+  u64 r = __ldg(L.l1 + (p >> 16)) + (u64)__ldg(L.l2 + (p >> l2_shift));
+  const u64 wb = (p >> l2_shift) << (l2_shift - 6);
+  const u64 we = p >> 6;
+  for (u64 w = wb; w < we; ++w) r += __popcll(__ldg(L.words + w));
+  const u32 rem = (u32)(p & 63);
+  if (rem) r += __popcll(wp & ((1ull << rem) - 1));
+  return r;
+}
+
+template <bool kOnes>
+__device__ __forceinline__ u64 select_dev(const LevelDev& L, u64 k, u32 l2_shift, u64 rate,
+                                          int rate_log) {
+  const u64* smp = kOnes ? L.ones : L.zeros;
+  const u64 ns = kOnes ? L.n_ones : L.n_zeros;
+  const u64 si = rate_log >= 0 ? (k >> rate_log) : k / rate;
+  u64 lo_pos = 0, hi_pos = L.n_bits - 1;
+  if (ns) {
+    if (si >= 1) lo_pos = __ldg(smp + (si - 1 < ns ? si - 1 : ns - 1));
+    if (si < ns) hi_pos = __ldg(smp + si);
+  }
+  u64 lo = lo_pos >> 16;
+  u64 hi = hi_pos >> 16;
+  if (hi > L.n_l1 - 1) hi = L.n_l1 - 1;
+  while (lo < hi) {
+    const u64 mid = (lo + hi + 1) >> 1;
+    const u64 c = __ldg(L.l1 + mid);
+    const u64 v = kOnes ? c : (mid << 16) - c;
+    if (v < k) lo = mid; else hi = mid - 1;
+  }
+  {
+    const u64 c = __ldg(L.l1 + lo);
+    k -= kOnes ? c : (lo << 16) - c;
+  }
+  const u64 per = 65536ull >> l2_shift;
+  const u64 base = lo * per;
+  u64 jl = base;
+  u64 jh = base + per < L.n_l2 ? base + per - 1 : L.n_l2 - 1;
+  while (jl < jh) {
+    const u64 mid = (jl + jh + 1) >> 1;
+    const u64 c = __ldg(L.l2 + mid);
+    const u64 v = kOnes ? c : ((mid - base) << l2_shift) - c;
+    if (v < k) jl = mid; else jh = mid - 1;
+  }
+  {
+    const u64 c = __ldg(L.l2 + jl);
+    k -= kOnes ? c : ((jl - base) << l2_shift) - c;
+  }
+  u64 w = jl << (l2_shift - 6);
+  while (true) {
+    u64 x = __ldg(L.words + w);
+    if (!kOnes) x = ~x;
+    const u32 pc = __popcll(x);
+    if (pc >= k) return (w << 6) + select_in_word64(x, (u32)k);
+    k -= pc;
+    ++w;
+  }
+}
+
+}  // namespace wt

@@ -79,6 +79,25 @@ __device__ __forceinline__ void st_release(u64* p, u64 v) {
 __device__ __forceinline__ void st_release32(u32* p, u32 v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Relaxed (gpu-scope, L1-bypassing, no fences): the look-back words carry
+// their value in the same 64/32-bit word as the flag, so no ordering with
+// other data is needed -- and acquire loads would invalidate L1 (CCTL.IVALL).
+__device__ __forceinline__ u64 ld_relaxed(const u64* p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u32 ld_relaxed32(const u32* p) {
+  u32 v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(u64* p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed32(u32* p, u32 v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // streaming 16-byte load that does not allocate in L1 (read-once data)
 __device__ __forceinline__ uint4 ld_stream16(const void* p) {
@@ -109,16 +128,16 @@ __device__ __forceinline__ u64 lookback_prefix(u64* status, u32 tile, u64 tile_t
   const int lane = threadIdx.x & 31;
   u64 prefix = 0;
   if (tile == 0) {
-    if (lane == 0) st_release(&status[0], WT_STATUS_FLAG_INC | tile_total);
+    if (lane == 0) st_relaxed(&status[0], WT_STATUS_FLAG_INC | tile_total);
     return 0;
   }
-  if (lane == 0) st_release(&status[tile], WT_STATUS_FLAG_AGG | tile_total);
+  if (lane == 0) st_relaxed(&status[tile], WT_STATUS_FLAG_AGG | tile_total);
   long long pred = (long long)tile - 1;
   while (true) {
     const long long idx = pred - lane;
-    u64 s = idx >= 0 ? ld_acquire(&status[idx]) : WT_STATUS_FLAG_INC;
+    u64 s = idx >= 0 ? ld_relaxed(&status[idx]) : WT_STATUS_FLAG_INC;
     while (__any_sync(0xffffffffu, (s >> 62) == 0)) {
-      if ((s >> 62) == 0) s = ld_acquire(&status[idx]);
+      if ((s >> 62) == 0) s = ld_relaxed(&status[idx]);
     }
     const u32 incm = __ballot_sync(0xffffffffu, (s >> 62) == 2);
     u64 val = WT_STATUS_VALUE(s);
@@ -131,7 +150,7 @@ __device__ __forceinline__ u64 lookback_prefix(u64* status, u32 tile, u64 tile_t
     prefix += warp_sum_u64(val);
     pred -= 32;
   }
-  if (lane == 0) st_release(&status[tile], WT_STATUS_FLAG_INC | (prefix + tile_total));
+  if (lane == 0) st_relaxed(&status[tile], WT_STATUS_FLAG_INC | (prefix + tile_total));
   return prefix;
 }
 

@@ -19,7 +19,22 @@ using namespace wt;
 // ---------------------------------------------------------------------------
 // errors
 // ---------------------------------------------------------------------------
+#include <chrono>
 static thread_local std::string g_err;
+// WT_TRACE=1: host-side phase timestamps of wt_construct on stderr
+static bool trace_on() {
+  static int v = -1;
+  if (v < 0) v = getenv("WT_TRACE") && getenv("WT_TRACE")[0] == '1';
+  return v == 1;
+}
+struct Tracer {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!trace_on()) return;
+    auto d = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[wt] %8.3f ms  %s\n", d, what);
+  }
+};
 static thread_local int64_t g_err_index = -1;
 
 static int fail(int code, const std::string& msg) {
@@ -197,6 +212,11 @@ struct LevelHost {
   u16* l2 = nullptr;
   u64* ones = nullptr;
   u64* zeros = nullptr;
+  // query-side rank-line layout (wt_qlayout.cu)
+  ulonglong2* lines = nullptr;
+  u32* sel1 = nullptr;
+  u32* sel0 = nullptr;
+  u64 n_lines = 0, sel_cap = 0;
 };
 
 struct wt_tree {
@@ -251,6 +271,16 @@ static void fill_treedev(wt_tree* t) {
     d.n_zeros = h.meta.n_zeros;
     d.n_l1 = h.meta.n_l1;
     d.n_l2 = h.meta.n_l2;
+    QLevelDev& q = D.ql[l];
+    q.lines = h.lines;
+    q.sel1 = h.sel1;
+    q.sel0 = h.sel0;
+    q.n_lines = h.n_lines;
+    q.n_bits = h.meta.n_bits;
+    q.total_ones = h.meta.total_ones;
+    q.n_sel1 = h.meta.total_ones ? ((h.meta.total_ones - 1) >> kQSelLog) + 1 : 0;
+    const u64 z = h.meta.n_bits - h.meta.total_ones;
+    q.n_sel0 = z ? ((z - 1) >> kQSelLog) + 1 : 0;
   }
   D.id_code = t->id_code;
   D.cum = t->cum;
@@ -283,6 +313,11 @@ static int alloc_tree(wt_tree* t, cudaStream_t st) {
     TRY(dalloc(&h.l2, h.meta.n_l2, st));
     TRY(dalloc(&h.ones, m / t->meta.sample_rate, st));
     TRY(dalloc(&h.zeros, m / t->meta.sample_rate, st));
+    h.n_lines = qlayout_lines(m);
+    h.sel_cap = (m >> kQSelLog) + 2;
+    TRY(dalloc(&h.lines, h.n_lines * 4, st));
+    TRY(dalloc(&h.sel1, h.sel_cap, st));
+    TRY(dalloc(&h.sel0, h.sel_cap, st));
   }
   TRY(dalloc(&t->nodes, P.nodes.size(), st));
   TRY(dalloc(&t->id_code, P.sigma, st));
@@ -305,9 +340,48 @@ static int alloc_tree(wt_tree* t, cudaStream_t st) {
   CU(cudaStreamSynchronize(st));  // host vectors above are temporaries
   uint64_t bytes = P.n_words * 8 + P.nodes.size() * sizeof(NodeEnt) + P.sigma * 14 + 8;
   for (auto& h : t->lv)
-    bytes += h.meta.n_l1 * 8 + h.meta.n_l2 * 2 + 2 * (h.meta.n_bits / t->meta.sample_rate) * 8;
+    bytes += h.meta.n_l1 * 8 + h.meta.n_l2 * 2 + 2 * (h.meta.n_bits / t->meta.sample_rate) * 8 +
+             h.n_lines * 64 + 2 * h.sel_cap * 4;
   t->meta.device_bytes = bytes;
   return WT_OK;
+}
+
+// query-side layout of every level; totals_dev[l] = ones of level l (device)
+static int launch_qlayouts(wt_tree* t, const u64* totals_dev, cudaStream_t st) {
+  const Plan& P = t->plan;
+  uint32_t sh = 0;
+  while ((1u << sh) < t->meta.l2_bits) ++sh;
+  for (uint32_t l = 0; l < P.L; ++l) {
+    LevelHost& h = t->lv[l];
+    LevelDev d{};
+    d.words = t->words + (P.offsets[l] >> 6);
+    d.l1 = h.l1;
+    d.l2 = h.l2;
+    d.n_bits = h.meta.n_bits;
+    d.n_l1 = h.meta.n_l1;
+    d.n_l2 = h.meta.n_l2;
+    CU(launch_qlayout(d, totals_dev + l, sh, h.lines, h.n_lines, h.sel1, h.sel_cap, h.sel0,
+                      h.sel_cap, st));
+  }
+  return WT_OK;
+}
+
+// host-known totals -> device, then the query layout (load / replicate paths)
+static int qlayouts_from_host_totals(wt_tree* t, cudaStream_t st) {
+  const Plan& P = t->plan;
+  if (!P.L) return WT_OK;
+  std::vector<u64> tot(P.L);
+  for (uint32_t l = 0; l < P.L; ++l) tot[l] = t->lv[l].meta.total_ones;
+  u64* d;
+  CU(cudaMalloc(&d, P.L * 8));
+  cudaError_t e = cudaMemcpyAsync(d, tot.data(), P.L * 8, cudaMemcpyHostToDevice, st);
+  int rc = e == cudaSuccess ? launch_qlayouts(t, d, st) : fail(WT_ERR_CUDA, cudaGetErrorString(e));
+  if (rc == WT_OK) {
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(WT_ERR_CUDA, cudaGetErrorString(e));
+  }
+  cudaFree(d);
+  return rc;
 }
 
 static void free_tree_arrays(wt_tree* t) {
@@ -321,6 +395,9 @@ static void free_tree_arrays(wt_tree* t) {
     F(h.l2);
     F(h.ones);
     F(h.zeros);
+    F(h.lines);
+    F(h.sel1);
+    F(h.sel0);
   }
   F(t->nodes);
   F(t->id_code);
@@ -391,6 +468,7 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
     CU(cudaEventCreate(&e0));
     CU(cudaEventCreate(&e1));
     struct EvGuard { cudaEvent_t a, b; ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); } } eg{e0, e1};
+    Tracer tr;
     CU(cudaEventRecord(e0, st));
     const void* dtext = text;
     if (!text_on_device) {
@@ -406,7 +484,9 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
     CU(launch_histogram(dtext, n, sym_bytes, dhist, sm_count(device), st));
     std::vector<uint64_t> hraw(nb);
     CU(cudaMemcpyAsync(hraw.data(), dhist, nb * 8, cudaMemcpyDeviceToHost, st));
+    tr.mark("histogram launched");
     CU(cudaStreamSynchronize(st));
+    tr.mark("histogram done");
 
     Plan& P = t->plan;
     if (alphabet) {
@@ -450,6 +530,7 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       if (P.symbols[i] < nb) P.hist[i] = (int64_t)hraw[P.symbols[i]];
     plan_codes(P);
     plan_shape(P, l2_bits);
+    tr.mark("plan done");
 
     t->meta.n = n;
     t->meta.sigma = P.sigma;
@@ -460,7 +541,21 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
     t->meta.first_coded = P.first_coded;
     t->meta.device = (uint32_t)device;
     t->meta.n_words = P.n_words;
+    {
+      // grow the stream-ordered pool once for the whole build (tree + scratch)
+      // instead of in many small steps; a no-op once the pool is warm
+      uint64_t est = P.n_words * 8 + 64ull * 1024 * 1024;
+      for (uint32_t l = 0; l < P.L; ++l) {
+        const uint64_t m = (uint64_t)P.sizes[l];
+        est += m / 7 + m / 32 + m / 256 + 2 * (m / sample_rate) * 8 + (m >> kQSelLog) * 8;
+        if (l == 1 || l == 2) est += m * P.code_bytes;
+      }
+      void* probe = nullptr;
+      if (cudaMallocAsync(&probe, est, st) == cudaSuccess) cudaFreeAsync(probe, st);
+      else cudaGetLastError();
+    }
     TRY(alloc_tree(t, st));
+    tr.mark("tree allocated");
 
     // raw symbol -> code LUT for level 0, unless the map is the identity
     std::vector<u16> lut(nb, 0);
@@ -555,11 +650,14 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       CU(launch_level(lp, in_bytes, P.code_bytes, l == 0 && dlut != nullptr, st));
       ci ^= 1;
     }
+    TRY(launch_qlayouts(t, totals, st));
+    tr.mark("levels launched");
     if (P.L) CU(cudaEventRecord(lev[P.L], st));
     CU(cudaEventRecord(e1, st));
     std::vector<uint64_t> tot(std::max<uint32_t>(P.L, 1));
     CU(cudaMemcpyAsync(tot.data(), totals, tot.size() * 8, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    tr.mark("build done");
     for (uint32_t l = 0; l < P.L; ++l) {
       wt_level_meta& m = t->lv[l].meta;
       m.total_ones = tot[l];
@@ -645,6 +743,7 @@ extern "C" int wt_tree_from_arrays(const wt_meta* meta, const uint16_t* symbols,
       o4 += m.n_zeros;
     }
     CU(cudaStreamSynchronize(st));
+    TRY(qlayouts_from_host_totals(t, st));
     fill_treedev(t);
     return WT_OK;
   };
@@ -1016,7 +1115,10 @@ extern "C" int wt_tree_replicate(wt_tree* root_tree, const uint8_t id[128], int 
   if (ms_out) cudaEventElapsedTime(ms_out, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  if (rank != 0) fill_treedev(t);
+  if (rank != 0) {
+    TRY(qlayouts_from_host_totals(t, st));
+    fill_treedev(t);
+  }
   *out = rank == 0 ? nullptr : t;
   return WT_OK;
 }

@@ -49,8 +49,23 @@ struct LevelDev {
   u64 n_bits, total_ones, n_ones, n_zeros, n_l1, n_l2;
 };
 
+// Query-side layout of one level ("rank lines"): 64-byte lines, word 0 =
+// ones before the line (absolute), words 1..7 = 448 bits of the level.  A
+// rank step touches exactly one line; select narrows to a few lines through
+// a line index per kQSel-th one / zero.  Built from the reference layout by
+// qlayout_kernel; exports keep the reference layout (wtree.py / bitvec.py).
+constexpr int kQBits = 448;
+constexpr int kQSelLog = 7;  // one select sample per 128 ones / zeros
+struct QLevelDev {
+  const ulonglong2* lines;  // 4 x 16 B per line
+  const u32* sel1;          // line holding the (j*128+1)-th one
+  const u32* sel0;
+  u64 n_lines, n_sel1, n_sel0, n_bits, total_ones;
+};
+
 struct TreeDev {
   LevelDev lv[kMaxLevels];
+  QLevelDev ql[kMaxLevels];
   const u32* id_code;    // code value | (len << 16), per symbol id
   const i64* cum;        // sigma + 1
   const u16* symbols;    // sigma, original symbol values

@@ -51,6 +51,11 @@ cudaError_t launch_query(const TreeDev& T, int kind, int out_kind, bool validate
                          const i64* args, void* out, u64 m, int rate_log, u64 base, u64* bad,
                          cudaStream_t st);
 
+// query-side rank-line layout (wt_qlayout.cu)
+u64 qlayout_lines(u64 n_bits);
+cudaError_t launch_qlayout(const LevelDev& L, const u64* total, u32 l2_shift, ulonglong2* lines,
+                           u64 n_lines, u32* sel1, u64 cap1, u32* sel0, u64 cap0, cudaStream_t st);
+
 // single bit-vector index (wt_bits.cu)
 struct BitsParams {
   const u64* words;

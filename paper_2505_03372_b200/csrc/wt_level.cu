@@ -61,6 +61,7 @@ struct LvSmem {
   u16 seg_ooff[LV_MAXSEG];
   u64 seg_zdst[LV_MAXSEG];
   u64 seg_odst[LV_MAXSEG];
+  u32 cnt[8];                    // fast path: next-level ones per (run, tile)
   u16 chunk_r1[LV_NT * LV_CPT];  // in-tile ones before each chunk
   u16 chunk_m[LV_NT * LV_CPT];   // level-bit mask of each chunk
   u16 lut[256];
@@ -247,6 +248,7 @@ __global__ void __launch_bounds__(LV_NT, 3) level_kernel(const LevelParams P) {
       mbar_wait(&sm.mbar[slot], (phase >> slot) & 1);
       phase ^= 1u << slot;
     }
+    if (tid < 8) sm.cnt[tid] = 0;
     if (tid == 0) {
       // remainder bytes the bulk copy could not take (last tile only)
       const u32 bulk = (valid * (u32)sizeof(TIn)) & ~15u;
@@ -331,6 +333,189 @@ __global__ void __launch_bounds__(LV_NT, 3) level_kernel(const LevelParams P) {
       }
     }
 
+    // ---- L2 entries and select samples (both paths) -------------------------
+    auto emit_directory = [&]() {
+    {
+      const u32 l2_mask = (1u << P.l2_log) - 1;
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        const u32 c = (u32)((warp * CPT + k) * 32 + lane);
+        const u64 g = t0 + (u64)c * CH;
+        if (g < P.m && (g & l2_mask) == 0) P.l2[g >> P.l2_log] = (u16)(P1 + r1c[k] - l1v);
+      }
+      // select samples: one warp per kind locates the sampled ordinals of
+      // the tile through the per-chunk prefix table (rankselect.py:509-532)
+      if (warp >= LV_NT / 32 - 2) {
+        const bool ones = warp == LV_NT / 32 - 1;
+        const u64 base = ones ? P1 : t0 - P1;             // ordinals before the tile
+        const u32 cnt = ones ? tile_ones : valid - tile_ones;
+        u64* out = ones ? P.ones : P.zeros;
+        const u64 cap = ones ? P.ones_cap : P.zeros_cap;
+        const u64 q0 = next_multiple(base, P.rate, P.rate_log);
+        for (u64 q = q0 + (u64)lane * P.rate; q <= base + cnt; q += 32 * P.rate) {
+          const u32 t = (u32)(q - base);  // 1-based ordinal inside the tile
+          u32 lo = 0, hi = LV_NT * CPT - 1;
+          while (lo < hi) {  // last chunk whose prefix is below t
+            const u32 mid = (lo + hi + 1) >> 1;
+            const u32 pre = ones ? sm.chunk_r1[mid] : mid * CH - sm.chunk_r1[mid];
+            if (pre < t) lo = mid; else hi = mid - 1;
+          }
+          const u32 pre = ones ? sm.chunk_r1[lo] : lo * CH - sm.chunk_r1[lo];
+          u32 mk = sm.chunk_m[lo];
+          if (!ones) {
+            const u32 e = lo * CH;
+            mk = ~mk & (valid - e >= (u32)CH ? (1u << CH) - 1 : (1u << (valid - e)) - 1);
+          }
+          const u64 sidx = (P.rate_log >= 0 ? (q >> P.rate_log) : q / P.rate) - 1;
+          if (sidx < cap) out[sidx] = t0 + lo * CH + __fns(mk, 0, (int)(t - pre));
+        }
+      }
+    }
+
+    };
+
+    if (scatter && single) {
+      // ---- fast path: the whole tile lies in one node ----------------------
+      // Both runs' destinations, staging offsets and next-level tile
+      // boundaries are computed redundantly by every thread (no run table).
+      const u32 tile_zeros = valid - tile_ones;
+      const NodeEnt* ne = P.nodes + sm.fkey;
+      const u64 zdst = (u64)__ldg(&ne->zero_base) + (t0 - P1);
+      const u64 odst = (u64)__ldg(&ne->one_base) + P1;
+      const u32 zoff = (u32)((zdst * SZ) & 15);
+      const u32 ooff = ((zoff + tile_zeros * SZ + 15) & ~15u) + (u32)((odst * SZ) & 15);
+      const bool zlive = tile_zeros && zdst < P.m_next;
+      const bool olive = tile_ones && odst < P.m_next;
+      const u32 zb1 = (u32)((zdst / NTILE + 1) * NTILE - zdst), zb2 = zb1 + NTILE;
+      const u32 ob1 = (u32)((odst / NTILE + 1) * NTILE - odst), ob2 = ob1 + NTILE;
+      const u32 sh1 = P.shift_bit - 1;
+      u32 cz0 = 0, cz1 = 0, cz2 = 0, co0 = 0, co1 = 0, co2 = 0;
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        const u32 c = (u32)((warp * CPT + k) * 32 + lane);
+        const u32 e = c * CH;
+        if (e >= valid) continue;
+        u32 cw[WPC];
+        load_chunk<TIn, TC, kLut>(in, c, valid, sm.lut, P.lut, cw);
+        const u32 m = msk[k];
+        u32 oslot = ooff + r1c[k] * SZ;
+        u32 zslot = zoff + (e - r1c[k]) * SZ;
+        if (e + CH <= valid) {
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const u32 v = elem<TC>(cw, j);
+            if (m & (1u << j)) {
+              *reinterpret_cast<TC*>(sm.stage + oslot) = (TC)v;
+              oslot += SZ;
+            } else {
+              *reinterpret_cast<TC*>(sm.stage + zslot) = (TC)v;
+              zslot += SZ;
+            }
+          }
+        } else {
+          for (int j = 0; j < CH && e + j < valid; ++j) {
+            const u32 v = elem<TC>(cw, j);
+            const u32 b = (m >> j) & 1u;
+            *reinterpret_cast<TC*>(sm.stage + (b ? oslot : zslot)) = (TC)v;
+            oslot += b * SZ;
+            zslot += (b ^ 1u) * SZ;
+          }
+        }
+        // next level's ones of this chunk, per run and destination tile
+        u32 m1 = 0;
+        constexpr int EPW = 4 / (int)SZ;
+#pragma unroll
+        for (int i = 0; i < WPC; ++i) m1 |= word_bits<TC>(cw[i], sh1) << (i * EPW);
+        const u32 vm = valid - e >= (u32)CH ? (1u << CH) - 1 : (1u << (valid - e)) - 1;
+        if (zlive) {
+          const u32 zm = ~m & vm, i0 = e - r1c[k], nz = __popc(zm);
+          const u32 hits = m1 & zm;
+          if (i0 + nz <= zb1) {
+            cz0 += __popc(hits);
+          } else if (i0 >= zb1 && i0 + nz <= zb2) {
+            cz1 += __popc(hits);
+          } else {  // a boundary falls inside this chunk's zeros
+            const u32 k1 = min(nz, zb1 > i0 ? zb1 - i0 : 0u), k2 = min(nz, zb2 > i0 ? zb2 - i0 : 0u);
+            const u32 b1m = k1 ? (k1 >= nz ? zm : zm & ((2u << __fns(zm, 0, (int)k1)) - 1)) : 0u;
+            const u32 b2m = k2 ? (k2 >= nz ? zm : zm & ((2u << __fns(zm, 0, (int)k2)) - 1)) : 0u;
+            cz0 += __popc(hits & b1m);
+            cz1 += __popc(hits & b2m & ~b1m);
+            cz2 += __popc(hits & ~b2m);
+          }
+        }
+        if (olive) {
+          const u32 om = m, i0 = r1c[k], no = __popc(om);
+          const u32 hits = m1 & om;
+          if (i0 + no <= ob1) {
+            co0 += __popc(hits);
+          } else if (i0 >= ob1 && i0 + no <= ob2) {
+            co1 += __popc(hits);
+          } else {
+            const u32 k1 = min(no, ob1 > i0 ? ob1 - i0 : 0u), k2 = min(no, ob2 > i0 ? ob2 - i0 : 0u);
+            const u32 b1m = k1 ? (k1 >= no ? om : om & ((2u << __fns(om, 0, (int)k1)) - 1)) : 0u;
+            const u32 b2m = k2 ? (k2 >= no ? om : om & ((2u << __fns(om, 0, (int)k2)) - 1)) : 0u;
+            co0 += __popc(hits & b1m);
+            co1 += __popc(hits & b2m & ~b1m);
+            co2 += __popc(hits & ~b2m);
+          }
+        }
+      }
+      fence_proxy_async();
+#pragma unroll
+      for (int d = 16; d; d >>= 1) {
+        cz0 += __shfl_xor_sync(FULL, cz0, d);
+        cz1 += __shfl_xor_sync(FULL, cz1, d);
+        cz2 += __shfl_xor_sync(FULL, cz2, d);
+        co0 += __shfl_xor_sync(FULL, co0, d);
+        co1 += __shfl_xor_sync(FULL, co1, d);
+        co2 += __shfl_xor_sync(FULL, co2, d);
+      }
+      if (lane == 0) {
+        if (cz0) atomicAdd(&sm.cnt[0], cz0);
+        if (cz1) atomicAdd(&sm.cnt[1], cz1);
+        if (cz2) atomicAdd(&sm.cnt[2], cz2);
+        if (co0) atomicAdd(&sm.cnt[3], co0);
+        if (co1) atomicAdd(&sm.cnt[4], co1);
+        if (co2) atomicAdd(&sm.cnt[5], co2);
+      }
+      __syncthreads();  // staged tile, counts and the chunk table complete
+      emit_directory();
+      if (warp == 0) {
+        u8* gout = reinterpret_cast<u8*>(P.out);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const bool live = r ? olive : zlive;
+          if (!live) continue;
+          const u32 cnt = r ? tile_ones : tile_zeros;
+          const u64 dst = r ? odst : zdst;
+          const u32 soff = r ? ooff : zoff;
+          const u32 bytes = cnt * SZ;
+          const u64 db = dst * SZ;
+          u32 head = (u32)((16 - (db & 15)) & 15);
+          if (head > bytes) head = bytes;
+          const u32 body = (bytes - head) & ~15u;
+          const u32 tail = bytes - head - body;
+          if (lane < (int)head) gout[db + lane] = sm.stage[soff + lane];
+          if (lane >= 16 && lane < 16 + (int)tail) {
+            const u32 o = head + body + (lane - 16);
+            gout[db + o] = sm.stage[soff + o];
+          }
+          if (lane == 0 && body) bulk_s2g(gout + db + head, sm.stage + soff + head, body);
+          if (lane == 1) {
+            const u64 tf = dst / NTILE;
+            const u32* cc = sm.cnt + 3 * r;
+            if (cc[0]) atomicAdd(P.next_counts + tf, cc[0]);
+            if (cc[1]) atomicAdd(P.next_counts + tf + 1, cc[1]);
+            if (cc[2]) atomicAdd(P.next_counts + tf + 2, cc[2]);
+          }
+        }
+        if (lane == 0) {
+          bulk_commit();
+          bulk_wait_read();
+        }
+      }
+    } else {
+    // ---- general path: several node segments, or the last level -------------
     // ---- 2c. node segments of the tile (only when it spans several nodes) ---
     u32 nseg = 1;
     if (scatter && !single) {
@@ -508,43 +693,7 @@ __global__ void __launch_bounds__(LV_NT, 3) level_kernel(const LevelParams P) {
       if (!direct) fence_proxy_async();
     }
 
-    // ---- 4. L2 entries and select samples ------------------------------------
-    {
-      const u32 l2_mask = (1u << P.l2_log) - 1;
-#pragma unroll
-      for (int k = 0; k < CPT; ++k) {
-        const u32 c = (u32)((warp * CPT + k) * 32 + lane);
-        const u64 g = t0 + (u64)c * CH;
-        if (g < P.m && (g & l2_mask) == 0) P.l2[g >> P.l2_log] = (u16)(P1 + r1c[k] - l1v);
-      }
-      // select samples: one warp per kind locates the sampled ordinals of
-      // the tile through the per-chunk prefix table (rankselect.py:509-532)
-      if (warp >= LV_NT / 32 - 2) {
-        const bool ones = warp == LV_NT / 32 - 1;
-        const u64 base = ones ? P1 : t0 - P1;             // ordinals before the tile
-        const u32 cnt = ones ? tile_ones : valid - tile_ones;
-        u64* out = ones ? P.ones : P.zeros;
-        const u64 cap = ones ? P.ones_cap : P.zeros_cap;
-        const u64 q0 = next_multiple(base, P.rate, P.rate_log);
-        for (u64 q = q0 + (u64)lane * P.rate; q <= base + cnt; q += 32 * P.rate) {
-          const u32 t = (u32)(q - base);  // 1-based ordinal inside the tile
-          u32 lo = 0, hi = LV_NT * CPT - 1;
-          while (lo < hi) {  // last chunk whose prefix is below t
-            const u32 mid = (lo + hi + 1) >> 1;
-            const u32 pre = ones ? sm.chunk_r1[mid] : mid * CH - sm.chunk_r1[mid];
-            if (pre < t) lo = mid; else hi = mid - 1;
-          }
-          const u32 pre = ones ? sm.chunk_r1[lo] : lo * CH - sm.chunk_r1[lo];
-          u32 mk = sm.chunk_m[lo];
-          if (!ones) {
-            const u32 e = lo * CH;
-            mk = ~mk & (valid - e >= (u32)CH ? (1u << CH) - 1 : (1u << (valid - e)) - 1);
-          }
-          const u64 sidx = (P.rate_log >= 0 ? (q >> P.rate_log) : q / P.rate) - 1;
-          if (sidx < cap) out[sidx] = t0 + lo * CH + __fns(mk, 0, (int)(t - pre));
-        }
-      }
-    }
+    emit_directory();
 
     // ---- 5. runs leave: bulk body per run, heads / tails by lanes; the next
     //         level's ones are counted per destination tile on the way ------
@@ -627,6 +776,7 @@ __global__ void __launch_bounds__(LV_NT, 3) level_kernel(const LevelParams P) {
         bulk_commit();
         bulk_wait_read();  // staging buffer reusable once the bulk reads are done
       }
+    }
     }
     __syncthreads();  // end of tile: input slot and staging buffer free
   }

@@ -40,16 +40,14 @@ __global__ void __launch_bounds__(Q_NT) access_kernel(const __grid_constant__ Tr
   u32 key = 0;
   int id = 0;
   for (u32 l = 0; l < T.L; ++l) {
-    const LevelDev& lv = T.lv[l];
-    const u64 w = __ldg(lv.words + (p >> 6));
-    const u32 bit = (u32)(w >> (p & 63)) & 1u;
-    const NodeEnt* ne = lv.nodes + key;
+    const NodeEnt* ne = T.lv[l].nodes + key;
+    u32 bit;
+    const u64 r1 = qrank1_bit(T.ql[l], p, bit);  // one 64-byte line per level
     const int leaf = __ldg(&ne->leaf[bit]);
     if (leaf >= 0) {
       id = leaf;
       break;
     }
-    const u64 r1 = rank1_with_word(lv, p, T.l2_shift, w);
     p = bit ? r1 + (u64)__ldg(&ne->one_base) : (p - r1) + (u64)__ldg(&ne->zero_base);
     key = (key << 1) | bit;
   }
@@ -94,12 +92,12 @@ __global__ void __launch_bounds__(Q_NT) rank_kernel(const __grid_constant__ Tree
   const u32 cd = __ldg(T.id_code + c);
   const u32 code = cd & 0xffffu, len = cd >> 16;
   for (u32 l = 0; l < len; ++l) {
-    const LevelDev& lv = T.lv[l];
     const u32 bit = (code >> (T.L - 1 - l)) & 1u;
     const u32 key = code >> (T.L - l);
-    const NodeEnt* ne = lv.nodes + key;
-    const u64 r1 = rank1_dev(lv, p, T.l2_shift);
-    p = bit ? r1 + (u64)__ldg(&ne->one_base) : (p - r1) + (u64)__ldg(&ne->zero_base);
+    const NodeEnt* ne = T.lv[l].nodes + key;
+    const u64 base = bit ? (u64)__ldg(&ne->one_base) : (u64)__ldg(&ne->zero_base);
+    const u64 r1 = qrank1(T.ql[l], p);
+    p = (bit ? r1 : p - r1) + base;
   }
   out[i] = (i64)(p - (u64)__ldg(T.cum + c));
 }
@@ -123,14 +121,13 @@ __global__ void __launch_bounds__(Q_NT) select_kernel(const __grid_constant__ Tr
   const u32 code = cd & 0xffffu, len = cd >> 16;
   u64 p = (u64)__ldg(T.cum + c) + (u64)k - 1;
   for (int l = (int)len - 1; l >= 0; --l) {
-    const LevelDev& lv = T.lv[l];
     const u32 bit = (code >> (T.L - 1 - l)) & 1u;
     const u32 key = code >> (T.L - l);
-    const NodeEnt* ne = lv.nodes + key;
+    const NodeEnt* ne = T.lv[l].nodes + key;
     if (bit)
-      p = select_dev<true>(lv, p - (u64)__ldg(&ne->one_base) + 1, T.l2_shift, T.rate, rate_log);
+      p = qselect<true>(T.ql[l], p - (u64)__ldg(&ne->one_base) + 1);
     else
-      p = select_dev<false>(lv, p - (u64)__ldg(&ne->zero_base) + 1, T.l2_shift, T.rate, rate_log);
+      p = qselect<false>(T.ql[l], p - (u64)__ldg(&ne->zero_base) + 1);
   }
   out[i] = (i64)p;
 }

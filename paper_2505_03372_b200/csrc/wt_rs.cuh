@@ -84,3 +84,100 @@ __device__ __forceinline__ u64 select_dev(const LevelDev& L, u64 k, u32 l2_shift
 }
 
 }  // namespace wt
+
+namespace wt {
+
+// ---------------------------------------------------------------------------
+// rank / select on the query-side rank-line layout (wt_qlayout.cu)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u64 qline_of(u64 p, u32& w) {
+  const u64 q = p >> 6;                                    // word index in the level
+  const u64 i = __umul64hi(q, 0x2492492492492493ull);      // q / 7 (exact for q < 2^61)
+  w = (u32)(q - 7 * i);
+  return i;
+}
+
+struct QLine {
+  u64 hdr;
+  u64 wd[7];
+};
+
+__device__ __forceinline__ QLine qload(const QLevelDev& Q, u64 i) {
+  const ulonglong2* L = Q.lines + i * 4;
+  const ulonglong2 a = __ldg(L), b = __ldg(L + 1), c = __ldg(L + 2), d = __ldg(L + 3);
+  QLine r;
+  r.hdr = a.x;
+  r.wd[0] = a.y; r.wd[1] = b.x; r.wd[2] = b.y; r.wd[3] = c.x; r.wd[4] = c.y; r.wd[5] = d.x;
+  r.wd[6] = d.y;
+  return r;
+}
+
+// ones in the line before word w, plus the word itself
+__device__ __forceinline__ u64 qline_prefix(const QLine& L, u32 w, u64& word) {
+  u64 r = L.hdr;
+  word = L.wd[0];
+#pragma unroll
+  for (int x = 0; x < 7; ++x) {
+    if ((u32)x < w) r += __popcll(L.wd[x]);
+    if ((u32)x == w) word = L.wd[x];
+  }
+  return r;
+}
+
+// rank1(p) for p in [0, n_bits] (the sentinel line makes p == n_bits work)
+__device__ __forceinline__ u64 qrank1(const QLevelDev& Q, u64 p) {
+  u32 w;
+  const u64 i = qline_of(p, w);
+  const QLine L = qload(Q, i);
+  u64 word;
+  const u64 r = qline_prefix(L, w, word);
+  const u32 rem = (u32)(p & 63);
+  return r + (rem ? __popcll(word & ((1ull << rem) - 1)) : 0);
+}
+
+// rank1(p) and the bit at p (p < n_bits): one line
+__device__ __forceinline__ u64 qrank1_bit(const QLevelDev& Q, u64 p, u32& bit) {
+  u32 w;
+  const u64 i = qline_of(p, w);
+  const QLine L = qload(Q, i);
+  u64 word;
+  const u64 r = qline_prefix(L, w, word);
+  const u32 rem = (u32)(p & 63);
+  bit = (u32)(word >> rem) & 1u;
+  return r + (rem ? __popcll(word & ((1ull << rem) - 1)) : 0);
+}
+
+template <bool kOnes>
+__device__ __forceinline__ u64 qselect(const QLevelDev& Q, u64 k) {
+  const u32* sel = kOnes ? Q.sel1 : Q.sel0;
+  const u64 ns = kOnes ? Q.n_sel1 : Q.n_sel0;
+  const u64 j = (k - 1) >> kQSelLog;
+  u64 lo = __ldg(sel + j);
+  u64 hi = j + 1 < ns ? (u64)__ldg(sel + j + 1) : Q.n_lines - 1;
+  while (lo < hi) {  // last line whose count before it is below k
+    const u64 mid = (lo + hi + 1) >> 1;
+    const u64 h = __ldg(reinterpret_cast<const u64*>(Q.lines + mid * 4));
+    const u64 v = kOnes ? h : mid * kQBits - h;
+    if (v < k) lo = mid; else hi = mid - 1;
+  }
+  const QLine L = qload(Q, lo);
+  k -= kOnes ? L.hdr : lo * kQBits - L.hdr;
+  u64 res = lo * kQBits;
+  bool done = false;
+#pragma unroll
+  for (int x = 0; x < 7; ++x) {
+    const u64 word = kOnes ? L.wd[x] : ~L.wd[x];
+    const u32 pc = __popcll(word);
+    if (!done) {
+      if (pc >= k) {
+        res += 64 * x + select_in_word64(word, (u32)k);
+        done = true;
+      } else {
+        k -= pc;
+      }
+    }
+  }
+  return res;
+}
+
+}  // namespace wt

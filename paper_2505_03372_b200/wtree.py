@@ -82,8 +82,17 @@ def _device_text(text):
 
 
 class _TreeHandle:
+    """Owns one ``wt_tree`` device handle.  Closures of the lazy host
+    mirrors capture this object, never the WaveletTree, so dropping the tree
+    frees device memory immediately (no reference cycle waiting for the GC)."""
+
     def __init__(self, h):
         self.h = h
+
+    def get(self, what: int, level: int, count: int, dtype) -> np.ndarray:
+        out = np.empty(int(count), dtype)
+        check(lib.wt_tree_get(self.h, what, level, ptr(out), out.nbytes), "wt_tree_get")
+        return out
 
     def __del__(self):
         if self.h:
@@ -125,8 +134,9 @@ class WaveletTree:
         self.level_sizes = self._get(_lib.A_LEVEL_SIZES, 0, L, np.int64)
         offsets = self._get(_lib.A_REGION_OFFS, 0, L, np.int64)
         n_words = int(meta.n_words)
+        hd = self._h
         self.bits = BitArray(None, offsets, self.level_sizes.copy(),
-                             fetch=lambda: self._get(_lib.A_WORDS, 0, n_words, np.uint64))
+                             fetch=lambda: hd.get(_lib.A_WORDS, 0, n_words, np.uint64))
         self._lmeta = []
         self.rs = []
         self.node_starts, self.node_rank0 = [], []
@@ -145,18 +155,17 @@ class WaveletTree:
         return self._h.h
 
     def _get(self, what: int, level: int, count: int, dtype) -> np.ndarray:
-        out = np.empty(int(count), dtype)
-        check(lib.wt_tree_get(self._h.h, what, level, ptr(out), out.nbytes), "wt_tree_get")
-        return out
+        return self._h.get(what, level, count, dtype)
 
     def _make_rs(self, l: int, lm) -> RankSelectIndex:
         handle = self._h
+        bits = self.bits
         sizes = {_lib.A_L1: (lm.n_l1, np.int64), _lib.A_L2: (lm.n_l2, np.uint16),
                  _lib.A_ONES: (lm.n_ones, np.int64), _lib.A_ZEROS: (lm.n_zeros, np.int64)}
 
         def fetch(what):
             n, dt = sizes[what]
-            return self._get(what, l, n, dt)
+            return handle.get(what, l, n, dt)
 
         def backend(kind, args):
             out = np.empty(len(args), np.int64)
@@ -165,7 +174,7 @@ class WaveletTree:
             return out
 
         return RankSelectIndex(self.params, lm, backend, fetch,
-                               lambda: self.bits.region_words(l), owner=handle)
+                               lambda: bits.region_words(l), owner=handle)
 
     def query(self, kind: int, ids, args, *, symbols: bool = False, access_ids: bool = False,
               chunk: int = 0):

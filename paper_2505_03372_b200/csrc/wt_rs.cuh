@@ -102,9 +102,29 @@ struct QLine {
   u64 wd[7];
 };
 
+// Random 64-byte line reads: hint the L2 to fetch 64 B (LTC64B) instead of
+// promoting the miss to a larger DRAM request -- every rank step is one
+// line, so anything beyond it is wasted HBM bandwidth.
+__device__ __forceinline__ ulonglong2 ld_line16(const ulonglong2* p) {
+  ulonglong2 v;
+  asm volatile("ld.global.nc.L2::64B.v2.u64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ u64 ld_u64_64b(const u64* p) {
+  u64 v;
+  asm volatile("ld.global.nc.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ u32 ld_u32_64b(const u32* p) {
+  u32 v;
+  asm volatile("ld.global.nc.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ QLine qload(const QLevelDev& Q, u64 i) {
   const ulonglong2* L = Q.lines + i * 4;
-  const ulonglong2 a = __ldg(L), b = __ldg(L + 1), c = __ldg(L + 2), d = __ldg(L + 3);
+  const ulonglong2 a = ld_line16(L), b = ld_line16(L + 1), c = ld_line16(L + 2),
+                   d = ld_line16(L + 3);
   QLine r;
   r.hdr = a.x;
   r.wd[0] = a.y; r.wd[1] = b.x; r.wd[2] = b.y; r.wd[3] = c.x; r.wd[4] = c.y; r.wd[5] = d.x;
@@ -152,11 +172,11 @@ __device__ __forceinline__ u64 qselect(const QLevelDev& Q, u64 k) {
   const u32* sel = kOnes ? Q.sel1 : Q.sel0;
   const u64 ns = kOnes ? Q.n_sel1 : Q.n_sel0;
   const u64 j = (k - 1) >> kQSelLog;
-  u64 lo = __ldg(sel + j);
-  u64 hi = j + 1 < ns ? (u64)__ldg(sel + j + 1) : Q.n_lines - 1;
+  u64 lo = ld_u32_64b(sel + j);
+  u64 hi = j + 1 < ns ? (u64)ld_u32_64b(sel + j + 1) : Q.n_lines - 1;
   while (lo < hi) {  // last line whose count before it is below k
     const u64 mid = (lo + hi + 1) >> 1;
-    const u64 h = __ldg(reinterpret_cast<const u64*>(Q.lines + mid * 4));
+    const u64 h = ld_u64_64b(reinterpret_cast<const u64*>(Q.lines + mid * 4));
     const u64 v = kOnes ? h : mid * kQBits - h;
     if (v < k) lo = mid; else hi = mid - 1;
   }

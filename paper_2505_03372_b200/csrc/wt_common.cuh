@@ -123,12 +123,22 @@ __device__ __forceinline__ uint4 ld_stream16(const void* p) {
   return v;
 }
 
-// position (0-based) of the k-th (1-based) set bit of a 64-bit word
+// position (0-based) of the k-th (1-based, k <= popc(w)) set bit of a word.
+// Branch-free popcount halving (the reference's select_in_word,
+// rankselect.py:59-80, halves the same way).  __fns is NOT one instruction on
+// sm_100a (ptxas expands it into a loop that dominated the select kernel).
+__device__ __forceinline__ u32 select_in_word32(u32 w, u32 k) {
+  u32 pos = 0, c, t;
+  c = __popc(w & 0xffffu); t = k > c ? 16u : 0u; k -= t ? c : 0u; w >>= t; pos += t;
+  c = __popc(w & 0xffu);   t = k > c ? 8u : 0u;  k -= t ? c : 0u; w >>= t; pos += t;
+  c = __popc(w & 0xfu);    t = k > c ? 4u : 0u;  k -= t ? c : 0u; w >>= t; pos += t;
+  c = __popc(w & 0x3u);    t = k > c ? 2u : 0u;  k -= t ? c : 0u; w >>= t; pos += t;
+  return pos + (k > (w & 1u) ? 1u : 0u);
+}
 __device__ __forceinline__ u32 select_in_word64(u64 w, u32 k) {
-  u32 lo = (u32)w;
-  u32 c = __popc(lo);
-  if (k > c) return 32 + __fns((u32)(w >> 32), 0, (int)(k - c));
-  return __fns(lo, 0, (int)k);
+  const u32 lo = (u32)w;
+  const u32 c = __popc(lo);
+  return k > c ? 32u + select_in_word32((u32)(w >> 32), k - c) : select_in_word32(lo, k);
 }
 
 __device__ __forceinline__ u64 warp_sum_u64(u64 v) {

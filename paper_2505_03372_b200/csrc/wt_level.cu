@@ -193,7 +193,7 @@ __device__ __forceinline__ void emit_samples(u64* __restrict__ out, u64 cap, u64
   if (q <= o0) q += ((o0 + 1 - q + rate - 1) / rate) * rate;
   for (; q <= o0 + cnt; q += rate) {
     const u64 s = (rate_log >= 0 ? (q >> rate_log) : q / rate) - 1;
-    if (s < cap) out[s] = pos0 + __fns(mask, 0, (int)(q - o0));
+    if (s < cap) out[s] = pos0 + select_in_word32(mask, (u32)(q - o0));
   }
 }
 
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(LV_NT, 3) level_kernel(const LevelParams P) {
             mk = ~mk & (valid - e >= (u32)CH ? (1u << CH) - 1 : (1u << (valid - e)) - 1);
           }
           const u64 sidx = (P.rate_log >= 0 ? (q >> P.rate_log) : q / P.rate) - 1;
-          if (sidx < cap) out[sidx] = t0 + lo * CH + __fns(mk, 0, (int)(t - pre));
+          if (sidx < cap) out[sidx] = t0 + lo * CH + select_in_word32(mk, t - pre);
         }
       }
     }
@@ -436,8 +436,8 @@ __global__ void __launch_bounds__(LV_NT, 3) level_kernel(const LevelParams P) {
             cz1 += __popc(hits);
           } else {  // a boundary falls inside this chunk's zeros
             const u32 k1 = min(nz, zb1 > i0 ? zb1 - i0 : 0u), k2 = min(nz, zb2 > i0 ? zb2 - i0 : 0u);
-            const u32 b1m = k1 ? (k1 >= nz ? zm : zm & ((2u << __fns(zm, 0, (int)k1)) - 1)) : 0u;
-            const u32 b2m = k2 ? (k2 >= nz ? zm : zm & ((2u << __fns(zm, 0, (int)k2)) - 1)) : 0u;
+            const u32 b1m = k1 ? (k1 >= nz ? zm : zm & ((2u << select_in_word32(zm, k1)) - 1)) : 0u;
+            const u32 b2m = k2 ? (k2 >= nz ? zm : zm & ((2u << select_in_word32(zm, k2)) - 1)) : 0u;
             cz0 += __popc(hits & b1m);
             cz1 += __popc(hits & b2m & ~b1m);
             cz2 += __popc(hits & ~b2m);
@@ -452,8 +452,8 @@ __global__ void __launch_bounds__(LV_NT, 3) level_kernel(const LevelParams P) {
             co1 += __popc(hits);
           } else {
             const u32 k1 = min(no, ob1 > i0 ? ob1 - i0 : 0u), k2 = min(no, ob2 > i0 ? ob2 - i0 : 0u);
-            const u32 b1m = k1 ? (k1 >= no ? om : om & ((2u << __fns(om, 0, (int)k1)) - 1)) : 0u;
-            const u32 b2m = k2 ? (k2 >= no ? om : om & ((2u << __fns(om, 0, (int)k2)) - 1)) : 0u;
+            const u32 b1m = k1 ? (k1 >= no ? om : om & ((2u << select_in_word32(om, k1)) - 1)) : 0u;
+            const u32 b2m = k2 ? (k2 >= no ? om : om & ((2u << select_in_word32(om, k2)) - 1)) : 0u;
             co0 += __popc(hits & b1m);
             co1 += __popc(hits & b2m & ~b1m);
             co2 += __popc(hits & ~b2m);

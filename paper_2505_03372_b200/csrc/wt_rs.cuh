@@ -4,9 +4,8 @@
 //        of the words between the L2 block start and p, masked last word;
 //        p == n_bits -> total_ones.
 // select: Alg. 2 (rankselect.py:229-367): sample window -> binary search over
-//        L1 -> binary search over L2 -> word scan -> in-word select (here one
-//        __fns instead of the popcount halving; the k-th set bit is unique so
-//        the answer is identical).
+//        L1 -> binary search over L2 -> word scan -> in-word select (popcount
+//        halving, select_in_word32 in wt_common.cuh).
 #pragma once
 #include "wt_common.cuh"
 

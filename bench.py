@@ -11,9 +11,9 @@ every rank answers its own 1e8 against a replica broadcast from rank 0 over
 NCCL).  The build of the C2 tree (single GPU, the other half of BASELINE.json's
 metric) is timed on rank 0 over the same K/W and reported under "build".
 
-``--impl reference`` times the reference algorithm's CPU port (oracle/, the
-reference itself is Python and cannot travel to the GPU box) on this host's
-cores for the same metric, on a bounded sample.
+``--impl reference`` times the reference itself (wtindex 0.1.0, installed
+unmodified into baseline/_ref; the oracle port when that is absent) on all of
+this host's cores for the same metric, on a bounded sample.
 """
 
 from __future__ import annotations
@@ -322,7 +322,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_port(seconds=args.cpu_seconds)
+        cpu = cpu_baseline(seconds=args.cpu_seconds)
 
     if world > 1:
         dist.barrier()
@@ -363,79 +363,99 @@ def traffic_from_profiles(kernel: str, launch_queries: int):
 
 
 # ---------------------------------------------------------------------------
-# CPU side: the reference algorithm's port (oracle/)
+# CPU side: the reference itself (baseline/_ref), else the oracle port
 # ---------------------------------------------------------------------------
-_CPU_TREE = None
-_CPU_Q = {}
+_CPU = {}
+
+
+def _reference_module():
+    """The unmodified reference (wtindex 0.1.0) installed into baseline/_ref
+    with pip; None when that install is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "wtindex")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import wtindex
+    import wtindex.cli
+    return wtindex
+
+
+def _cpu_setup(n_log: int, num: int, seed: int):
+    """Build the C2-recipe tree at n = 2^n_log and pre-generate `num` queries
+    of each kind with the reference CLI's generator (cli.py:246-260)."""
+    text = np.random.default_rng(0).integers(0, 256, 1 << n_log, dtype=np.uint8)
+    wt = _reference_module()
+    t0 = time.perf_counter()
+    if wt is not None:
+        tree = wt.construct(text)
+        build_s = time.perf_counter() - t0
+        qs = {k: wt.cli._bench_queries(tree, k, num, seed) for k in ("access", "rank", "select")}
+        kind = "reference"
+    else:
+        import oracle as O
+        tree = O.build(text)
+        build_s = time.perf_counter() - t0
+        qs = {k: O.bench_queries(tree.n, tree.hist, k, num, seed)
+              for k in ("access", "rank", "select")}
+        kind = "port"
+    _CPU.update(tree=tree, qs=qs, kind=kind, wt=wt)
+    return build_s, kind
 
 
 def _cpu_worker(job):
-    """Answer one slice of a pre-generated batch with the port; returns seconds."""
-    kind, lo, hi, seed, n_q = job
-    t = _CPU_TREE
-    if kind in _CPU_Q:
-        ids, args = _CPU_Q[kind]
-    else:
-        import oracle as O
-        ids, args = O.bench_queries(t.n, t.hist, kind, n_q, seed)
-    ids = None if ids is None else ids[lo:hi]
-    args = args[lo:hi]
+    """Answer queries [lo, hi) of one kind; returns seconds."""
+    kind, lo, hi = job
+    tree, q, wt = _CPU["tree"], _CPU["qs"][kind], _CPU["wt"]
     t0 = time.perf_counter()
-    if kind == "access":
-        t.access_ids(args)
-    elif kind == "rank":
-        t.rank_ids(ids, args)
+    if wt is not None:   # the reference's own batch path (batch.py:152-239)
+        sub = wt.QueryBatch(kind, q.args[lo:hi], None if q.symbols is None else q.symbols[lo:hi])
+        wt.BatchRunner(tree, sub.chunk_size, 1).run(sub)
     else:
-        t.select_ids(ids, args)
+        ids, args = q
+        ids = None if ids is None else ids[lo:hi]
+        if kind == "access":
+            tree.access_ids(args[lo:hi])
+        elif kind == "rank":
+            tree.rank_ids(ids, args[lo:hi])
+        else:
+            tree.select_ids(ids, args[lo:hi])
     return time.perf_counter() - t0
 
 
-def cpu_baseline_port(seconds: float = 20.0, n_log: int = 22, procs: int = 1):
-    """Time the oracle port: build (n = 2^n_log, sigma = 256) and mixed queries."""
-    global _CPU_TREE
-    import oracle as O
-    text = np.random.default_rng(0).integers(0, 256, 1 << n_log, dtype=np.uint8)
-    t0 = time.perf_counter()
-    _CPU_TREE = O.build(text)
-    build_s = time.perf_counter() - t0
+def cpu_baseline(seconds: float = 20.0, n_log: int = 22):
+    """Rank 0 at N=1: the reference on ONE host core, bounded sample."""
     n_q = 30000
+    build_s, kind = _cpu_setup(n_log, n_q, 0)
     done, spent = 0, 0.0
-    seed = 0
     while spent < seconds * 0.5 and done < 3_000_000:
-        for kind in ("access", "rank", "select"):
-            spent += _cpu_worker((kind, 0, n_q, seed, n_q))
+        for k in ("access", "rank", "select"):
+            spent += _cpu_worker((k, 0, n_q))
             done += n_q
-        seed += 1
-    return {"value": done / spent, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"oracle port (numpy restatement of wtindex), tree n=2^{n_log} sigma=256, "
-                      f"{done} mixed queries in 30k-query kind-homogeneous batches",
+    what = ("wtindex 0.1.0 (the reference, baseline/_ref) access_batch/rank_batch/select_batch"
+            if kind == "reference" else "oracle port (numpy restatement of wtindex)")
+    return {"value": done / spent, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{what}, tree n=2^{n_log} sigma=256, {done} mixed queries in "
+                      f"{n_q}-query kind-homogeneous batches, 1 process",
             "build_symbols_per_s": (1 << n_log) / build_s}
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm (CPU port) on all host cores."""
+    """--impl reference: the reference's CPU path on all host cores."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    global _CPU_TREE
     import multiprocessing as mp
-
-    import oracle as O
     n_log = args.ref_n_log
-    text = np.random.default_rng(0).integers(0, 256, 1 << n_log, dtype=np.uint8)
-    t0 = time.perf_counter()
-    _CPU_TREE = O.build(text)
-    build_s = time.perf_counter() - t0
     procs = os.cpu_count() or 1
     per_proc = args.ref_queries_per_proc
-    for kind in ("access", "rank", "select"):   # generated before the pool forks
-        _CPU_Q[kind] = O.bench_queries(_CPU_TREE.n, _CPU_TREE.hist, kind, procs * per_proc, 7)
+    build_s, kind = _cpu_setup(n_log, procs * per_proc, 7)   # before the pool forks
     ctx = mp.get_context("fork")
     times = []
     with ctx.Pool(procs) as pool:
         for step in range(args.warmup + args.steps):
-            jobs = [(kind, p * per_proc, (p + 1) * per_proc, 0, 0)
-                    for p in range(procs) for kind in ("access", "rank", "select")]
+            jobs = [(k, p * per_proc, (p + 1) * per_proc)
+                    for p in range(procs) for k in ("access", "rank", "select")]
             t0 = time.perf_counter()
             pool.map(_cpu_worker, jobs)
             dt = time.perf_counter() - t0
@@ -444,9 +464,11 @@ def run_reference(args):
     q = procs * per_proc * 3
     ms = float(np.mean(times)) * 1e3
     value = q / (ms / 1e3)
-    sample = (f"oracle port (numpy restatement of wtindex; the Python reference cannot travel "
-              f"to the GPU box), tree n=2^{n_log} sigma=256 built in {build_s:.1f}s, "
-              f"{q} mixed queries per step over {procs} processes")
+    what = ("wtindex 0.1.0, the unmodified reference installed in baseline/_ref, through "
+            "BatchRunner.run" if kind == "reference" else
+            "oracle port (numpy restatement of wtindex; baseline/_ref absent)")
+    sample = (f"{what}; tree n=2^{n_log} sigma=256 (C2 recipe) built in {build_s:.1f}s; "
+              f"{q} mixed queries per step (cli._bench_queries) over {procs} processes")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
@@ -455,7 +477,7 @@ def run_reference(args):
         "data": "synthetic (seeded PCG64, cli._bench_queries recipe)",
         "config": {"workload": f"C2 recipe at n=2^{n_log} (bounded CPU sample), mixed "
                                "access/rank/select", "n": 1 << n_log, "sigma": 256},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": kind,
                          "sample": sample, "build_symbols_per_s": (1 << n_log) / build_s},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))

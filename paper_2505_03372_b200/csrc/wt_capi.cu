@@ -579,16 +579,12 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       if (next_w > end_w) CU(cudaMemsetAsync(t->words + end_w, 0, (next_w - end_w) * 8, st));
     }
 
-    uint64_t max_tiles = 1;
-    for (uint32_t l = 0; l < P.L; ++l)
-      max_tiles = std::max<uint64_t>(
-          max_tiles, level_tiles((uint64_t)P.sizes[l], l == 0 ? sym_bytes : P.code_bytes));
-    u32* counts[2];
-    u64* prefix;
+    uint32_t l2_log = 0;
+    while ((1u << l2_log) < l2_bits) ++l2_log;
+    std::vector<cudaEvent_t> lev(P.L + 1);
+    for (auto& e : lev) CU(cudaEventCreate(&e));
+    struct EvVec { std::vector<cudaEvent_t>& v; ~EvVec() { for (auto e : v) cudaEventDestroy(e); } } evg{lev};
     u64* totals;
-    TRY(S.get(&counts[0], max_tiles + 4));
-    TRY(S.get(&counts[1], max_tiles + 4));
-    TRY(S.get(&prefix, max_tiles + 1));
     TRY(S.get(&totals, std::max<uint32_t>(P.L, 1)));
     CU(cudaMemsetAsync(totals, 0, std::max<uint32_t>(P.L, 1) * 8, st));
     void* cur[2] = {nullptr, nullptr};
@@ -602,11 +598,74 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       TRY(S.get(&p, (uint64_t)P.sizes[2] * P.code_bytes + 16));
       cur[1] = p;
     }
-    uint32_t l2_log = 0;
-    while ((1u << l2_log) < l2_bits) ++l2_log;
-    std::vector<cudaEvent_t> lev(P.L + 1);
-    for (auto& e : lev) CU(cudaEventCreate(&e));
-    struct EvVec { std::vector<cudaEvent_t>& v; ~EvVec() { for (auto e : v) cudaEventDestroy(e); } } evg{lev};
+    static const bool cta_levels = getenv("WT_LEVEL_CTA") != nullptr;  // A/B: old CTA-tile kernel
+    if (!cta_levels) {
+      // K2w: warp tiles; per-tile and per-L1-block ones counts of each level
+      // come from the previous level's scatter (level 0: a counting pass)
+      uint64_t max_tiles = 1, max_l1 = 1;
+      for (uint32_t l = 0; l < P.L; ++l) {
+        max_tiles = std::max<uint64_t>(
+            max_tiles, wlevel_tiles((uint64_t)P.sizes[l], l == 0 ? sym_bytes : P.code_bytes));
+        max_l1 = std::max<uint64_t>(max_l1, t->lv[l].meta.n_l1);
+      }
+      u32 *tcnt[2], *l1cnt[2];
+      for (int i = 0; i < 2; ++i) {
+        TRY(S.get(&tcnt[i], max_tiles + 64));
+        TRY(S.get(&l1cnt[i], max_l1 + 4));
+      }
+      if (P.L && P.sizes[0]) {
+        CU(cudaMemsetAsync(l1cnt[0], 0, (t->lv[0].meta.n_l1 + 4) * 4, st));
+        CU(launch_wcount0(dtext, n, sym_bytes, dlut, P.L - 1, tcnt[0], l1cnt[0], sm_count(device), st));
+      }
+      int ci = 0;
+      for (uint32_t l = 0; l < P.L; ++l) {
+        const uint64_t m = (uint64_t)P.sizes[l];
+        CU(cudaEventRecord(lev[l], st));
+        if (m == 0) continue;
+        const int in_bytes = l == 0 ? sym_bytes : P.code_bytes;
+        LevelHost& h = t->lv[l];
+        CU(launch_l1_scan(l1cnt[ci], h.meta.n_l1, h.l1, totals + l, st));
+        WLevelParams wp{};
+        wp.in = l == 0 ? dtext : cur[(l - 1) & 1];
+        wp.out = l + 1 < P.L ? cur[l & 1] : nullptr;
+        wp.m = m;
+        wp.m_next = l + 1 < P.L ? (uint64_t)P.sizes[l + 1] : 0;
+        if (wp.out && wp.m_next == 0) wp.out = nullptr;
+        if (wp.out) {
+          const uint64_t nt = wlevel_tiles(wp.m_next, P.code_bytes);
+          CU(cudaMemsetAsync(tcnt[ci ^ 1], 0, (nt + 64) * 4, st));
+          CU(cudaMemsetAsync(l1cnt[ci ^ 1], 0, (t->lv[l + 1].meta.n_l1 + 4) * 4, st));
+        }
+        wp.words = t->words + (P.offsets[l] >> 6);
+        wp.l2 = h.l2;
+        wp.ones = h.ones;
+        wp.zeros = h.zeros;
+        wp.ones_cap = m / sample_rate;
+        wp.zeros_cap = m / sample_rate;
+        wp.nodes = t->nodes + P.node_off[l];
+        wp.lut = l == 0 ? dlut : nullptr;
+        wp.l1 = h.l1;
+        wp.tile_counts = tcnt[ci];
+        wp.next_tile_counts = tcnt[ci ^ 1];
+        wp.next_l1_counts = l1cnt[ci ^ 1];
+        wp.shift_bit = P.L - 1 - l;
+        wp.shift_key = P.L - l;
+        wp.l2_log = l2_log;
+        wp.rate_log = rate_log_of(sample_rate);
+        wp.rate = sample_rate;
+        CU(launch_wlevel(wp, in_bytes, P.code_bytes, l == 0 && dlut != nullptr, sm_count(device), st));
+        ci ^= 1;
+      }
+    } else {
+    uint64_t max_tiles = 1;
+    for (uint32_t l = 0; l < P.L; ++l)
+      max_tiles = std::max<uint64_t>(
+          max_tiles, level_tiles((uint64_t)P.sizes[l], l == 0 ? sym_bytes : P.code_bytes));
+    u32* counts[2];
+    u64* prefix;
+    TRY(S.get(&counts[0], max_tiles + 4));
+    TRY(S.get(&counts[1], max_tiles + 4));
+    TRY(S.get(&prefix, max_tiles + 1));
     if (P.L && P.sizes[0]) {
       const uint32_t tiles0 = level_tiles((uint64_t)P.sizes[0], sym_bytes);
       CU(cudaMemsetAsync(counts[0], 0, (size_t)(tiles0 + 4) * 4, st));
@@ -649,6 +708,7 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       lp.rate = sample_rate;
       CU(launch_level(lp, in_bytes, P.code_bytes, l == 0 && dlut != nullptr, st));
       ci ^= 1;
+    }
     }
     TRY(launch_qlayouts(t, totals, st));
     tr.mark("levels launched");

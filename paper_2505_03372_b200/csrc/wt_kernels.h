@@ -37,6 +37,36 @@ cudaError_t launch_tile_scan(const u32* counts, u32 tiles, int tiles_per_l1, u64
                              u64* l1, u64 n_l1, u64* total, cudaStream_t st);
 int level_tiles_per_l1(int in_bytes);
 
+// K2w parameters (wt_wlevel.cu): warp-granular tiles of 2 KB of input
+struct WLevelParams {
+  const void* in;          // level input: text (level 0) or the partitioned codes
+  void* out;               // next level's codes (nullptr at the last level)
+  u64 m, m_next;           // level_sizes[l], level_sizes[l+1]
+  u64* words;              // region start
+  u16* l2;
+  u64* ones;
+  u64* zeros;
+  u64 ones_cap, zeros_cap;
+  const NodeEnt* nodes;    // 2^l entries keyed by the l-bit code prefix
+  const u16* lut;          // level 0: raw symbol -> code (nullptr: identity)
+  const u64* l1;           // this level's L1 directory (ones before each 65536-bit block)
+  const u32* tile_counts;  // ones per warp tile of this level
+  u32* next_tile_counts;   // ones of level l+1 per warp tile of level l+1 (atomics)
+  u32* next_l1_counts;     // ones of level l+1 per L1 block (atomics)
+  u32 shift_bit;           // L-1-l
+  u32 shift_key;           // L-l
+  u32 l2_log;
+  int rate_log;            // log2(rate) when rate is a power of two, else -1
+  u64 rate;
+};
+cudaError_t launch_wlevel(const WLevelParams& p, int in_bytes, int code_bytes, bool lut, int sms,
+                          cudaStream_t st);
+u32 wlevel_tiles(u64 m, int in_bytes);
+cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, const u16* lut, u32 shift_bit,
+                           u32* tile_counts, u32* l1_counts, int sms, cudaStream_t st);
+// exclusive scan of per-L1-block counts -> l1[0..n_l1) and the level total
+cudaError_t launch_l1_scan(const u32* counts, u64 n_l1, u64* l1, u64* total, cudaStream_t st);
+
 // K1: raw-symbol histogram (wt_hist.cu); hist must be zeroed (u64[256|65536])
 cudaError_t launch_histogram(const void* text, u64 n, int sym_bytes, u64* hist, int sms,
                              cudaStream_t st);

@@ -32,7 +32,10 @@
 
 namespace wt {
 
-constexpr int LV_NT = 256;
+#ifndef WT_LV_NT
+#define WT_LV_NT 256
+#endif
+constexpr int LV_NT = WT_LV_NT;
 constexpr int LV_CPT = 4;      // 16-byte input chunks per thread per tile
 constexpr int LV_MAXSEG = 64;  // node segments per tile staged; more -> direct stores
 constexpr int LV_SEGPAD = 48;  // staging slack per segment (two 16-byte alignments)
@@ -199,7 +202,7 @@ __device__ __forceinline__ void emit_samples(u64* __restrict__ out, u64 cap, u64
 
 // ---------------------------------------------------------------------------
 template <typename TIn, typename TC, bool kLut>
-__global__ void __launch_bounds__(LV_NT, 3) level_kernel(const LevelParams P) {
+__global__ void __launch_bounds__(LV_NT, 768 / LV_NT) level_kernel(const LevelParams P) {
   using S = LvShape<TIn>;
   constexpr int CH = S::CH, TILE = S::TILE, CPT = LV_CPT;
   constexpr int WPC = CH * (int)sizeof(TC) / 4;

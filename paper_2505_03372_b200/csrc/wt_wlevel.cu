@@ -1,0 +1,892 @@
+// wt_wlevel.cu -- K2w: one fused pass per wavelet-tree level, WARP-granular tiles.
+//
+// Replaces, for level l, the reference's
+//   stable_sort_by_prefix  (wtree.py:92-100)        -> one-pass stable per-node partition
+//   fill_level / fill_region / _pack_span (wtree.py:103-107, bitvec.py:119-151)
+//   build_index (rankselect.py:442-536): L2 entries and select samples
+//   (L1 entries come from the per-L1-block scan that precedes the launch)
+//
+// Every warp owns whole 2 KB tiles (2048 u8 / 1024 u16 elements) and never
+// waits for another warp: no __syncthreads anywhere.  Per tile:
+//   0. the NEXT tile's 2 KB are already in flight into registers (4 x 16 B
+//      per lane, streaming loads issued one tile ahead);
+//   1. SWAR bit extraction -> one mask per 16-byte chunk, packed warp scans of
+//      the ones; the mask is the tile's bit-vector words (u16 / u8 stores);
+//   2. P1 (ones before the tile) = L1 prefix of its 65536-bit block + the
+//      counts of the block's earlier tiles (counted by the previous level);
+//   3. single-node tile (the common case): every element goes to a
+//      warp-private staging buffer at its place in the zeros run or the ones
+//      run (offsets congruent to the global destination mod 16); lanes 16..31
+//      walk their chunk from the middle so the two lanes sharing a bank never
+//      store in the same step; each run body leaves as ONE cp.async.bulk
+//      shared -> global store, heads / tails by lanes;
+//   4. the staged runs are scanned (SWAR) for the ones of the NEXT level's
+//      bit per next-level tile / L1 block (a few atomics per run): this is
+//      what makes step 2 possible for the next level without a look-back;
+//   5. L2 entries and select samples from (P1, in-tile prefix).
+// Multi-node tiles (node boundaries inside the tile) store element by element.
+// Destination of element j with bit b in node `key`:
+//   b=1: one_base[key] + R1(j)        b=0: zero_base[key] + R0(j)
+#include "wt_common.cuh"
+#include "wt_kernels.h"
+
+namespace wt {
+namespace {
+
+constexpr int W_NT = 128;
+constexpr int W_WARPS = W_NT / 32;
+constexpr int W_BYTES = 2048;  // input bytes per warp tile
+constexpr int W_K = 4;         // 16-byte chunks per lane per tile
+#ifndef WT_W_RING
+#define WT_W_RING 2
+#endif
+constexpr int W_RING = WT_W_RING;  // input tiles in flight per warp
+constexpr unsigned FULLM = 0xffffffffu;
+
+template <typename TIn>
+struct WS {
+  static constexpr int CH = 16 / (int)sizeof(TIn);         // elements per chunk
+  static constexpr int TILE = W_BYTES / (int)sizeof(TIn);  // 2048 | 1024
+  static constexpr int TPL1 = kL1Bits / TILE;              // 32 | 64 tiles per L1 block
+};
+template <typename TIn, typename TC>
+struct WStage {
+  static constexpr int BYTES = WS<TIn>::TILE * (int)sizeof(TC) + 64;
+};
+
+__device__ __forceinline__ u32 smem_addr(const void* p) {
+  return (u32)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void w_bulk_s2g(void* dst, const void* src, u32 bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_addr(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void w_bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void w_bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void w_bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void w_fence_proxy() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// bit `sh` of every element of WPC packed code words -> LSB-first mask
+template <typename TC, int WPC>
+__device__ __forceinline__ u32 wmask(const u32 (&cw)[WPC], u32 sh) {
+  u32 m = 0;
+  if (sizeof(TC) == 1) {
+    // two words (8 elements) per multiply: bits at 8b (word 0) and 8b+4
+    // (word 1) gather to bits 24..31 in element order
+#pragma unroll
+    for (int i = 0; i + 1 < WPC; i += 2) {
+      const u32 y0 = (cw[i] >> sh) & 0x01010101u;
+      const u32 y1 = (cw[i + 1] >> sh) & 0x01010101u;
+      const u32 z = y1 * 16u + y0;
+      m |= ((z * 0x01020408u) >> 24) << (4 * i);
+    }
+    if (WPC & 1) {
+      const u32 y = (cw[WPC - 1] >> sh) & 0x01010101u;
+      m |= ((y * 0x01020408u) >> 24) << (4 * (WPC - 1));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < WPC; ++i) {
+      const u32 y = (cw[i] >> sh) & 0x00010001u;
+      m |= ((y | (y >> 15)) & 3u) << (2 * i);
+    }
+  }
+  return m;
+}
+
+template <typename TC, int WPC>
+__device__ __forceinline__ u32 welem(const u32 (&cw)[WPC], int j) {
+  if (sizeof(TC) == 1) return (cw[j >> 2] >> ((j & 3) * 8)) & 0xffu;
+  return (cw[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+}
+
+// 16 input bytes -> WPC code words (level 0 maps raw symbols through the LUT)
+template <typename TIn, typename TC, bool kLut, int WPC>
+__device__ __forceinline__ void wcodes(const uint4& q, const u16* slut, const u16* glut,
+                                       u32 (&cw)[WPC]) {
+  const u32 qw[4] = {q.x, q.y, q.z, q.w};
+  if (!kLut) {
+#pragma unroll
+    for (int i = 0; i < WPC; ++i) cw[i] = qw[i];
+  } else {
+    constexpr int CH = 16 / (int)sizeof(TIn);
+#pragma unroll
+    for (int i = 0; i < WPC; ++i) cw[i] = 0;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const u32 raw = sizeof(TIn) == 1 ? (qw[j >> 2] >> ((j & 3) * 8)) & 0xffu
+                                       : (qw[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+      const u32 code = sizeof(TIn) == 1 ? (u32)slut[raw] : (u32)__ldg(glut + raw);
+      if (sizeof(TC) == 1)
+        cw[j >> 2] |= code << ((j & 3) * 8);
+      else
+        cw[j >> 1] |= code << ((j & 1) * 16);
+    }
+  }
+}
+
+__device__ __forceinline__ uint4 w_load16(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// load one tile's 4 chunks per lane; bytes beyond the level are zero
+template <typename TIn>
+__device__ __forceinline__ void wload(const u8* in, u64 m, u32 t, int lane, uint4 (&q)[W_K]) {
+  using S = WS<TIn>;
+  const u64 t0 = (u64)t * S::TILE;
+  const u8* base = in + t0 * sizeof(TIn);
+  if (t0 + S::TILE <= m) {
+#pragma unroll
+    for (int k = 0; k < W_K; ++k) q[k] = w_load16(base + (k * 32 + lane) * 16);
+  } else {
+    const u64 bytes = (m - t0) * sizeof(TIn);
+#pragma unroll
+    for (int k = 0; k < W_K; ++k) {
+      const u32 o = (u32)(k * 32 + lane) * 16;
+      if (o + 16 <= bytes) {
+        q[k] = w_load16(base + o);
+      } else {
+        u32 w[4] = {0, 0, 0, 0};
+        for (u32 b = o; b < bytes && b < o + 16; ++b) w[(b - o) >> 2] |= (u32)base[b] << (8 * ((b - o) & 3));
+        q[k] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ u64 wnext_multiple(u64 o, u64 rate, int rate_log) {
+  if (rate_log >= 0) return ((o >> rate_log) + 1) << rate_log;
+  return (o / rate + 1) * rate;
+}
+
+}  // namespace
+
+// Any tile the fast path does not take (the level's partial last tile, tiles
+// spanning several nodes): loads from global memory, element-by-element
+// destination stores, per-element next-level counts.
+template <typename TIn, typename TC, bool kLut>
+__device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u16* slut) {
+  using S = WS<TIn>;
+  constexpr int CH = S::CH, TILE = S::TILE, TPL1 = S::TPL1;
+  constexpr int WPC = CH * (int)sizeof(TC) / 4;
+  constexpr int NTILE_LOG = sizeof(TC) == 1 ? 11 : 10;
+  const int lane = threadIdx.x & 31;
+  const bool scatter = P.out != nullptr;
+  const u8* in = reinterpret_cast<const u8*>(P.in);
+  const u32 l2_chunks = (1u << P.l2_log) / CH;
+  uint4 q[W_K];
+  wload<TIn>(in, P.m, t, lane, q);
+  u32 cw[W_K][WPC];
+#pragma unroll
+  for (int k = 0; k < W_K; ++k) wcodes<TIn, TC, kLut, WPC>(q[k], slut, P.lut, cw[k]);
+    const u64 t0 = (u64)t * TILE;
+    const u32 valid = (u32)min((u64)TILE, P.m - t0);
+    // ---- P1: ones before the tile ------------------------------------------
+    const u32 b = t / TPL1;
+    const u32 tb = t - b * TPL1;  // tiles of the block before this one
+    u32 pre = 0;
+#pragma unroll
+    for (int r = 0; r < TPL1 / 32; ++r) {
+      const u32 j = r * 32 + lane;
+      if (j < tb) pre += __ldg(P.tile_counts + b * TPL1 + j);
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) pre += __shfl_xor_sync(FULLM, pre, d);
+    const u64 l1v = __ldg(P.l1 + b);
+    const u64 P1 = l1v + pre;
+
+    // ---- 1. codes, masks, in-tile scan ---------------------------------------
+    u32 msk[W_K];
+#pragma unroll
+    for (int k = 0; k < W_K; ++k) {
+      u32 mk = wmask<TC, WPC>(cw[k], P.shift_bit);
+      const u32 e = (u32)(k * 32 + lane) * CH;
+      if (e + CH > valid) mk &= e >= valid ? 0u : (1u << (valid - e)) - 1u;
+      msk[k] = mk;
+    }
+    u32 r1c[W_K], ktot[W_K];
+#pragma unroll
+    for (int k = 0; k < W_K; k += 2) {
+      const u32 x = (u32)__popc(msk[k]) | ((u32)__popc(msk[k + 1]) << 16);
+      u32 inc = x;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u32 y = __shfl_up_sync(FULLM, inc, d);
+        if (lane >= d) inc += y;
+      }
+      const u32 tot = __shfl_sync(FULLM, inc, 31);
+      const u32 ex = inc - x;
+      r1c[k] = ex & 0xffffu;
+      r1c[k + 1] = ex >> 16;
+      ktot[k] = tot & 0xffffu;
+      ktot[k + 1] = tot >> 16;
+    }
+    u32 tile_ones = 0;
+#pragma unroll
+    for (int k = 0; k < W_K; ++k) {
+      r1c[k] += tile_ones;
+      tile_ones += ktot[k];
+    }
+
+    // ---- bit-vector words -----------------------------------------------------
+#pragma unroll
+    for (int k = 0; k < W_K; ++k) {
+      const u32 e = (u32)(k * 32 + lane) * CH;
+      if (e < ((valid + 63u) & ~63u)) {  // through the level's last word: padding stays zero
+        const u64 bit = t0 + e;
+        if (CH == 16)
+          reinterpret_cast<u16*>(P.words)[bit >> 4] = (u16)msk[k];
+        else
+          reinterpret_cast<u8*>(P.words)[bit >> 3] = (u8)msk[k];
+      }
+    }
+
+    // ---- L2 entries ----------------------------------------------------------
+    if (l2_chunks <= 32) {
+      if ((lane & (l2_chunks - 1)) == 0) {
+#pragma unroll
+        for (int k = 0; k < W_K; ++k) {
+          const u32 e = (u32)(k * 32 + lane) * CH;
+          if (e < valid) P.l2[(t0 + e) >> P.l2_log] = (u16)(P1 + r1c[k] - l1v);
+        }
+      }
+    } else if (lane == 0) {
+      const u64 l2m = (1ull << P.l2_log) - 1;
+#pragma unroll
+      for (int k = 0; k < W_K; ++k) {
+        const u64 g = t0 + (u64)k * 32 * CH;
+        if (g < P.m && (g & l2m) == 0) P.l2[g >> P.l2_log] = (u16)(P1 + r1c[k] - l1v);
+      }
+    }
+
+    // ---- select samples (rankselect.py:509-532) ------------------------------
+#pragma unroll
+    for (int kind = 0; kind < 2; ++kind) {
+      const bool ones = kind == 0;
+      const u64 base = ones ? P1 : t0 - P1;
+      const u32 cnt = ones ? tile_ones : valid - tile_ones;
+      u64* out = ones ? P.ones : P.zeros;
+      const u64 cap = ones ? P.ones_cap : P.zeros_cap;
+      for (u64 qo = wnext_multiple(base, P.rate, P.rate_log); qo <= base + cnt; qo += P.rate) {
+        const u32 tt = (u32)(qo - base);  // 1-based ordinal inside the tile
+        u32 kk = W_K - 1, acc = 0;  // k-row holding ordinal tt
+#pragma unroll
+        for (int k = 0; k < W_K; ++k) {
+          const int rv = (int)valid - k * 32 * CH;
+          const u32 row_valid = rv <= 0 ? 0u : (rv >= 32 * CH ? 32u * CH : (u32)rv);
+          const u32 kc = ones ? ktot[k] : row_valid - ktot[k];
+          if (tt <= acc + kc) { kk = k; break; }
+          acc += kc;
+        }
+        // lane owning ordinal tt within k-row kk
+        u32 pre_l = 0, cnt_l = 0, mk = 0;
+#pragma unroll
+        for (int k = 0; k < W_K; ++k) {
+          if ((u32)k == kk) {
+            const u32 e = (u32)(k * 32 + lane) * CH;
+            const u32 vm = e >= valid ? 0u : (e + CH <= valid ? (CH == 16 ? 0xffffu : 0xffu)
+                                                              : (1u << (valid - e)) - 1u);
+            mk = ones ? msk[k] : (~msk[k] & vm);
+            pre_l = ones ? r1c[k] : (u32)(k * 32 + lane) * CH - r1c[k];
+            cnt_l = __popc(mk);
+          }
+        }
+        const u32 own = __ballot_sync(FULLM, pre_l < tt && tt <= pre_l + cnt_l);
+        if (own && lane == __ffs(own) - 1) {
+          const u64 s = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
+          if (s < cap) out[s] = t0 + (u64)(kk * 32 + lane) * CH + select_in_word32(mk, tt - pre_l);
+        }
+      }
+    }
+
+    if (!scatter) return;
+
+    {
+      TC* gout = reinterpret_cast<TC*>(P.out);
+      const u32 sh1 = P.shift_bit - 1;
+#pragma unroll
+      for (int k = 0; k < W_K; ++k) {
+        const u32 e = (u32)(k * 32 + lane) * CH;
+        u32 r1 = r1c[k];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          if (e + j < valid) {
+            const u32 v = welem<TC, WPC>(cw[k], j);
+            const NodeEnt* ne = P.nodes + (v >> P.shift_key);
+            const u32 bt = (msk[k] >> j) & 1u;
+            const u64 dst = bt ? (u64)__ldg(&ne->one_base) + P1 + r1
+                               : (u64)__ldg(&ne->zero_base) + (t0 + e + j - P1 - r1);
+            if (dst < P.m_next) {
+              gout[dst] = (TC)v;
+              if ((v >> sh1) & 1u) {
+                atomicAdd(P.next_tile_counts + (dst >> NTILE_LOG), 1u);
+                atomicAdd(P.next_l1_counts + (dst >> 16), 1u);
+              }
+            }
+            r1 += bt;
+          }
+        }
+      }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// the kernel: full single-node tiles take the fast path below
+// ---------------------------------------------------------------------------
+// Fast-path layout: a tile is 8 rows of 256 input bytes; lane i owns bytes
+// [8i, 8i + 8) of every row (CR = 8 / sizeof(TIn) elements).  Lane regions in
+// a staged run then span ~128 bytes per row step, so the byte stores of one
+// step fall in distinct banks.
+template <typename TIn, typename TC>
+struct WF {
+  static constexpr int CR = 8 / (int)sizeof(TIn);            // elements per lane per row
+  static constexpr int RE = 256 / (int)sizeof(TIn);          // elements per row
+  static constexpr int ROWS = W_BYTES / 256;                 // 8
+  static constexpr int WR = CR * (int)sizeof(TC) / 4;        // code words per lane-row
+  static constexpr int STAGE = ((WS<TIn>::TILE * (int)sizeof(TC) + 64) + 127) & ~127;
+  static constexpr int WARP_SMEM = W_RING * W_BYTES + 2 * STAGE + 64;  // ring, stages, mbarriers
+};
+
+__device__ __forceinline__ void w_mbar_init(u64* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
+}
+__device__ __forceinline__ void w_load_tile(void* dst, const void* src, u64* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(W_BYTES)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(W_BYTES), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void w_mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// codes of one lane-row (8 input bytes) -> WR words
+template <typename TIn, typename TC, bool kLut>
+__device__ __forceinline__ void wrow_codes(uint2 v, const u16* slut, const u16* glut,
+                                           u32 (&cw)[WF<TIn, TC>::WR]) {
+  constexpr int WR = WF<TIn, TC>::WR;
+  if (!kLut) {
+    cw[0] = v.x;
+    if (WR > 1) cw[WR - 1] = v.y;
+  } else {
+    constexpr int CR = WF<TIn, TC>::CR;
+    const u32 qw[2] = {v.x, v.y};
+#pragma unroll
+    for (int i = 0; i < WR; ++i) cw[i] = 0;
+#pragma unroll
+    for (int j = 0; j < CR; ++j) {
+      const u32 raw = sizeof(TIn) == 1 ? (qw[j >> 2] >> ((j & 3) * 8)) & 0xffu
+                                       : (qw[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+      const u32 code = sizeof(TIn) == 1 ? (u32)slut[raw] : (u32)__ldg(glut + raw);
+      if (sizeof(TC) == 1)
+        cw[j >> 2] |= code << ((j & 3) * 8);
+      else
+        cw[j >> 1] |= code << ((j & 1) * 16);
+    }
+  }
+}
+
+template <typename TC>
+__device__ __forceinline__ void st_shared(u32 addr, u32 v) {
+  if (sizeof(TC) == 1)
+    asm("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+  else
+    asm("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+}
+
+// SWAR count of bit `sh` of every code in a 16-byte chunk
+template <typename TC>
+__device__ __forceinline__ u32 wswar16(uint4 v, u32 sh) {
+  if (sizeof(TC) == 1) {
+    const u32 y = ((v.x >> sh) & 0x01010101u) + ((v.y >> sh) & 0x01010101u) +
+                  ((v.z >> sh) & 0x01010101u) + ((v.w >> sh) & 0x01010101u);
+    return (y * 0x01010101u) >> 24;
+  }
+  const u32 y = ((v.x >> sh) & 0x00010001u) + ((v.y >> sh) & 0x00010001u) +
+                ((v.z >> sh) & 0x00010001u) + ((v.w >> sh) & 0x00010001u);
+  return (y * 0x00010001u) >> 16;
+}
+
+// next-level ones of one staged run (elements [0, cnt) at stage byte soff),
+// per next-level tile (a run spans at most 3) and L1 block.  Returns the
+// three counts (lanes hold the sums): prefix counts up to the tile boundaries
+// b1, b2 give the split.  16-byte aligned chunks fully inside the run are
+// counted with SWAR; the few elements outside them (run head / tail) and the
+// parts of the chunks holding b1 / b2 are counted one element per lane.
+template <typename TC>
+__device__ __forceinline__ void wcount_run3(const u8* stage, u32 soff, u32 cnt, u32 b1, u32 b2,
+                                            u32 sh1, int lane, u32& ca, u32& cp1, u32& cp2) {
+  constexpr u32 SZ = sizeof(TC);
+  constexpr u32 EPC = 16 / SZ;
+  const u32 h = min(cnt, ((16u - (soff & 15u)) & 15u) / SZ);  // head elements
+  const u32 nfull = (cnt - h) / EPC;
+  const u32 ts = h + nfull * EPC;                               // tail start
+  const u8* base = stage + soff;
+  for (u32 c = lane; c < nfull; c += 32) {
+    const u32 i0 = h + c * EPC;
+    const u32 x = wswar16<TC>(*reinterpret_cast<const uint4*>(base + i0 * SZ), sh1);
+    ca += x;
+    cp1 += i0 + EPC <= b1 ? x : 0u;
+    cp2 += i0 + EPC <= b2 ? x : 0u;
+  }
+  // element-wise: lanes 0..15 head, 16..31 tail (count toward ca, cp1, cp2)
+  {
+    const u32 k = lane & 15;
+    const u32 i = lane < 16 ? k : ts + k;
+    const bool in = lane < 16 ? k < h : i < cnt;
+    const u32 v = in ? (SZ == 1 ? (u32)base[i] : (u32)reinterpret_cast<const u16*>(base)[i]) : 0u;
+    const u32 bt = in ? (v >> sh1) & 1u : 0u;
+    ca += bt;
+    cp1 += i < b1 ? bt : 0u;
+    cp2 += i < b2 ? bt : 0u;
+  }
+  // element-wise: the part before b1 (lanes 0..15) / b2 (lanes 16..31) of
+  // the full chunk holding that boundary (those chunks were not added)
+  {
+    const u32 bb = lane < 16 ? b1 : b2;
+    const bool strad = bb > h && bb < ts && ((bb - h) % EPC) != 0;
+    const u32 cs = strad ? h + ((bb - h) / EPC) * EPC : 0u;
+    const u32 i = cs + (lane & 15);
+    const bool in = strad && i < bb;
+    const u32 v = in ? (SZ == 1 ? (u32)base[i] : (u32)reinterpret_cast<const u16*>(base)[i]) : 0u;
+    const u32 bt = in ? (v >> sh1) & 1u : 0u;
+    if (lane < 16) cp1 += bt; else cp2 += bt;
+  }
+}
+
+template <typename TIn, typename TC, bool kLut>
+__global__ void __launch_bounds__(W_NT) wlevel_kernel(const __grid_constant__ WLevelParams P) {
+  using S = WS<TIn>;
+  using F = WF<TIn, TC>;
+  constexpr int TILE = S::TILE, TPL1 = S::TPL1;
+  constexpr int CR = F::CR, RE = F::RE, ROWS = F::ROWS, WR = F::WR;
+  constexpr u32 SZ = sizeof(TC);
+  constexpr int NTILE_LOG = sizeof(TC) == 1 ? 11 : 10;  // next level's tile (input = codes)
+  extern __shared__ __align__(128) u8 smem_raw[];
+  u16* slut = reinterpret_cast<u16*>(smem_raw);  // 256 entries (u8 text + LUT)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  u8* wbase = smem_raw + 512 + warp * F::WARP_SMEM;
+  u8* ring = wbase;
+  u8* stage0 = wbase + W_RING * W_BYTES;
+  u64* mbar = reinterpret_cast<u64*>(wbase + W_RING * W_BYTES + 2 * F::STAGE);
+
+  if (kLut && sizeof(TIn) == 1) {
+    for (int i = tid; i < 256; i += W_NT) slut[i] = P.lut[i];
+    __syncthreads();
+  }
+  const u32 ntiles = (u32)((P.m + TILE - 1) / TILE);
+  const u32 nfull = (u32)(P.m / TILE);
+  const u32 gw = blockIdx.x * W_WARPS + warp, nw = gridDim.x * W_WARPS;
+  const bool scatter = P.out != nullptr;
+  const u8* in = reinterpret_cast<const u8*>(P.in);
+
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < W_RING; ++i) w_mbar_init(&mbar[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < W_RING; ++i) {
+      const u32 t = gw + i * nw;
+      if (t < nfull) w_load_tile(ring + i * W_BYTES, in + (u64)t * W_BYTES, &mbar[i]);
+    }
+  }
+  __syncwarp();
+
+  u32 it = 0;
+  for (u32 t = gw; t < ntiles; t += nw, ++it) {
+    const u32 slot = it % W_RING;
+    if (t >= nfull) {  // the partial last tile
+      general_tile<TIn, TC, kLut>(P, t, slut);
+      if (scatter && lane == 0) w_bulk_commit();  // keep one bulk group per tile
+      continue;
+    }
+    const u8* tin = ring + slot * W_BYTES;
+    // ---- P1 (loads go out before the tile data is waited on) -----------------
+    const u32 b = t / TPL1;
+    const u32 tb = t - b * TPL1;
+    u32 pre = 0;
+#pragma unroll
+    for (int r = 0; r < TPL1 / 32; ++r) {
+      const u32 j = r * 32 + lane;
+      if (j < tb) pre += __ldg(P.tile_counts + b * TPL1 + j);
+    }
+    const u64 l1v = __ldg(P.l1 + b);
+    const u64 t0 = (u64)t * TILE;
+    w_mbar_wait(&mbar[slot], (it / W_RING) & 1);
+
+    // ---- single node? (first and last element of the tile) -------------------
+    u32 fcode, lcode;
+    {
+      const u32 f = sizeof(TIn) == 1 ? (u32)tin[0] : (u32)reinterpret_cast<const u16*>(tin)[0];
+      const u32 l = sizeof(TIn) == 1 ? (u32)tin[TILE - 1]
+                                     : (u32)reinterpret_cast<const u16*>(tin)[TILE - 1];
+      fcode = !kLut ? f : sizeof(TIn) == 1 ? (u32)slut[f] : (u32)__ldg(P.lut + f);
+      lcode = !kLut ? l : sizeof(TIn) == 1 ? (u32)slut[l] : (u32)__ldg(P.lut + l);
+    }
+    const u32 fkey = fcode >> P.shift_key;
+    if (scatter && fkey != (lcode >> P.shift_key)) {
+      __syncwarp();
+      if (lane == 0 && t + W_RING * nw < nfull)
+        w_load_tile(ring + slot * W_BYTES, in + (u64)(t + W_RING * nw) * W_BYTES, &mbar[slot]);
+      general_tile<TIn, TC, kLut>(P, t, slut);
+      if (lane == 0) w_bulk_commit();  // keep one bulk group per tile
+      continue;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) pre += __shfl_xor_sync(FULLM, pre, d);
+    const u64 P1 = l1v + pre;
+
+    // ---- pass 1: masks and counts per row ------------------------------------
+    u32 mrow[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const uint2 v = *reinterpret_cast<const uint2*>(tin + r * 256 + lane * 8);
+      u32 cw[WR];
+      wrow_codes<TIn, TC, kLut>(v, slut, P.lut, cw);
+      mrow[r] = wmask<TC, WR>(cw, P.shift_bit);
+    }
+    u32 r1[ROWS], rtot[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; r += 2) {
+      const u32 x = (u32)__popc(mrow[r]) | ((u32)__popc(mrow[r + 1]) << 16);
+      u32 inc = x;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u32 y = __shfl_up_sync(FULLM, inc, d);
+        if (lane >= d) inc += y;
+      }
+      const u32 tot = __shfl_sync(FULLM, inc, 31);
+      const u32 ex = inc - x;
+      r1[r] = ex & 0xffffu;
+      r1[r + 1] = ex >> 16;
+      rtot[r] = tot & 0xffffu;
+      rtot[r + 1] = tot >> 16;
+    }
+    u32 tile_ones = 0;
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      r1[r] += tile_ones;
+      tile_ones += rtot[r];
+    }
+
+    // ---- bit-vector words: each lane-row mask is CR bits at t0 + r*RE + lane*CR
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      if (CR == 8) {
+        reinterpret_cast<u8*>(P.words)[(t0 >> 3) + r * (RE / 8) + lane] = (u8)mrow[r];
+      } else {  // 4 bits: pair lanes into bytes
+        const u32 nb = __shfl_down_sync(FULLM, mrow[r], 1);
+        if (!(lane & 1))
+          reinterpret_cast<u8*>(P.words)[(t0 >> 3) + r * (RE / 8) + (lane >> 1)] =
+              (u8)(mrow[r] | (nb << 4));
+      }
+    }
+
+    // ---- L2 entries: blocks start at lane-row boundaries (l2_bits >= 64) ------
+    if ((1u << P.l2_log) >= (u32)RE) {  // at most one per row: lane r handles row r
+      u32 rs = 0;  // ones before row `lane` (= r1 of lane 0 in that row)
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) {
+        const u32 v = __shfl_sync(FULLM, r1[r], 0);
+        rs = lane == r ? v : rs;
+      }
+      const u64 g = t0 + (u64)lane * RE;
+      if (lane < ROWS && (((u32)g) & ((1u << P.l2_log) - 1)) == 0)
+        P.l2[g >> P.l2_log] = (u16)(P1 + rs - l1v);
+    } else if (((lane * CR) & ((1u << P.l2_log) - 1)) == 0) {  // same lanes in every row
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r)
+        P.l2[(t0 + r * RE + lane * CR) >> P.l2_log] = (u16)(P1 + r1[r] - l1v);
+    }
+
+    // ---- select samples (rankselect.py:509-532) --------------------------------
+#pragma unroll
+    for (int kind = 0; kind < 2; ++kind) {
+      const bool ones = kind == 0;
+      const u64 base = ones ? P1 : t0 - P1;
+      const u32 cnt = ones ? tile_ones : TILE - tile_ones;
+      u64* out = ones ? P.ones : P.zeros;
+      const u64 cap = ones ? P.ones_cap : P.zeros_cap;
+      const u64 q0 = wnext_multiple(base, P.rate, P.rate_log);
+      if (q0 > base + cnt) continue;
+      for (u64 qo = q0; qo <= base + cnt; qo += P.rate) {
+        const u32 tt = (u32)(qo - base);  // 1-based ordinal inside the tile
+        u32 pre_l = 0, mk = 0, rr = 0;
+        bool own = false;
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+          const u32 pl = ones ? r1[r] : (u32)(r * RE + lane * CR) - r1[r];
+          const u32 mr = ones ? mrow[r] : (~mrow[r] & ((1u << CR) - 1u));
+          if (!own && pl < tt && tt <= pl + __popc(mr)) {
+            own = true;
+            pre_l = pl;
+            mk = mr;
+            rr = r;
+          }
+        }
+        if (own) {
+          const u64 sidx = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
+          if (sidx < cap) out[sidx] = t0 + rr * RE + lane * CR + select_in_word32(mk, tt - pre_l);
+        }
+      }
+    }
+
+    if (scatter) {
+      // ---- pass 2: stable partition into the staged zeros / ones runs ----------
+      u8* stage = stage0 + (it & 1) * F::STAGE;
+      const u32 sbase = smem_addr(stage);
+      if (it >= 2) {
+        if (lane == 0) w_bulk_wait_read1();  // the bulk store that last read this buffer
+        __syncwarp();
+      }
+      const u32 tile_zeros = TILE - tile_ones;
+      const NodeEnt* ne = P.nodes + fkey;
+      const u64 zdst = (u64)__ldg(&ne->zero_base) + (t0 - P1);
+      const u64 odst = (u64)__ldg(&ne->one_base) + P1;
+      const u32 zoff = (u32)((zdst * SZ) & 15);
+      const u32 ooff = ((zoff + tile_zeros * SZ + 15) & ~15u) + (u32)((odst * SZ) & 15);
+      const bool zlive = tile_zeros && zdst < P.m_next;
+      const bool olive = tile_ones && odst < P.m_next;
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) {
+        const uint2 v = *reinterpret_cast<const uint2*>(tin + r * 256 + lane * 8);
+        u32 cw[WR];
+        wrow_codes<TIn, TC, kLut>(v, slut, P.lut, cw);
+        const u32 m = mrow[r];
+        u32 oa = sbase + ooff + r1[r] * SZ;
+        u32 za = sbase + zoff + ((u32)(r * RE + lane * CR) - r1[r]) * SZ;
+#pragma unroll
+        for (int j = 0; j < CR; ++j) {
+          // st.shared.u8/u16 keep the low bits: no masking of the element
+          const u32 val = sizeof(TC) == 1 ? cw[j >> 2] >> ((j & 3) * 8) : cw[j >> 1] >> ((j & 1) * 16);
+          if (m & (1u << j)) {
+            st_shared<TC>(oa, val);
+            oa += SZ;
+          } else {
+            st_shared<TC>(za, val);
+            za += SZ;
+          }
+        }
+      }
+      w_fence_proxy();
+      __syncwarp();
+      // the input slot is free: the tile three ahead streams into it
+      if (lane == 0 && t + W_RING * nw < nfull)
+        w_load_tile(ring + slot * W_BYTES, in + (u64)(t + W_RING * nw) * W_BYTES, &mbar[slot]);
+      u8* gout = reinterpret_cast<u8*>(P.out);
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const bool live = rr ? olive : zlive;
+        if (!live) continue;
+        const u32 cnt = rr ? tile_ones : tile_zeros;
+        const u64 dst = rr ? odst : zdst;
+        const u32 soff = rr ? ooff : zoff;
+        const u32 bytes = cnt * SZ;
+        const u64 db = dst * SZ;
+        u32 head = (u32)((16 - (db & 15)) & 15);
+        if (head > bytes) head = bytes;
+        const u32 body = (bytes - head) & ~15u;
+        const u32 tail = bytes - head - body;
+        if (lane < (int)head) gout[db + lane] = stage[soff + lane];
+        if (lane >= 16 && lane < 16 + (int)tail) {
+          const u32 o2 = head + body + (lane - 16);
+          gout[db + o2] = stage[soff + o2];
+        }
+        if (lane == 0 && body) w_bulk_s2g(gout + db + head, stage + soff + head, body);
+        // next level's ones of this run per next-level tile (<= 3) and L1 block
+        const u64 t_first = dst >> NTILE_LOG;
+        const u32 b1 = min(cnt, (u32)(((t_first + 1) << NTILE_LOG) - dst));
+        const u32 b2 = min(cnt, b1 + (1u << NTILE_LOG));
+        u32 ca = 0, cp1 = 0, cp2 = 0;
+        wcount_run3<TC>(stage, soff, cnt, b1, b2, P.shift_bit - 1, lane, ca, cp1, cp2);
+        u32 pk = cp1 | (cp2 << 16);  // counts <= 4096 fit in 16 bits
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+          ca += __shfl_xor_sync(FULLM, ca, d);
+          pk += __shfl_xor_sync(FULLM, pk, d);
+        }
+        if (lane < 3) {
+          const u32 p1 = pk & 0xffffu, p2 = pk >> 16;
+          const u32 cc = lane == 0 ? p1 : lane == 1 ? p2 - p1 : ca - p2;
+          if (cc) {
+            const u64 tf = t_first + lane;
+            atomicAdd(P.next_tile_counts + tf, cc);
+            atomicAdd(P.next_l1_counts + ((tf << NTILE_LOG) >> 16), cc);
+          }
+        }
+      }
+      if (lane == 0) w_bulk_commit();  // one bulk group per scattering fast tile
+    } else {
+      __syncwarp();
+      if (lane == 0 && t + W_RING * nw < nfull)
+        w_load_tile(ring + slot * W_BYTES, in + (u64)(t + W_RING * nw) * W_BYTES, &mbar[slot]);
+    }
+  }
+  if (scatter && lane == 0) w_bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------
+// level 0: ones per warp tile of the text's top code bit (streaming pass)
+// ---------------------------------------------------------------------------
+template <typename TIn, bool kLut>
+__global__ void __launch_bounds__(W_NT) wcount0_kernel(const TIn* __restrict__ text, u64 n,
+                                                      const u16* __restrict__ lut, u32 shift_bit,
+                                                      u32* __restrict__ tile_counts,
+                                                      u32* __restrict__ l1_counts) {
+  using S = WS<TIn>;
+  constexpr int CH = S::CH;
+  __shared__ u16 slut[kLut && sizeof(TIn) == 1 ? 256 : 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (kLut && sizeof(TIn) == 1) {
+    for (int i = tid; i < 256; i += W_NT) slut[i] = lut[i];
+    __syncthreads();
+  }
+  const u32 ntiles = (u32)((n + S::TILE - 1) / S::TILE);
+  for (u32 t = blockIdx.x * W_WARPS + warp; t < ntiles; t += gridDim.x * W_WARPS) {
+    uint4 q[W_K];
+    wload<TIn>(reinterpret_cast<const u8*>(text), n, t, lane, q);
+    const u64 t0 = (u64)t * S::TILE;
+    u32 cnt = 0;
+#pragma unroll
+    for (int k = 0; k < W_K; ++k) {
+      const u32 e = (u32)(k * 32 + lane) * CH;
+      const u32 qw[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        if (t0 + e + j >= n) break;
+        const u32 raw = sizeof(TIn) == 1 ? (qw[j >> 2] >> ((j & 3) * 8)) & 0xffu
+                                         : (qw[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+        const u32 code = !kLut ? raw : sizeof(TIn) == 1 ? (u32)slut[raw] : (u32)__ldg(lut + raw);
+        cnt += (code >> shift_bit) & 1u;
+      }
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(FULLM, cnt, d);
+    if (lane == 0) {
+      tile_counts[t] = cnt;
+      if (cnt) atomicAdd(l1_counts + (t / S::TPL1), cnt);
+    }
+  }
+}
+
+// one CTA: exclusive scan of per-L1-block counts -> the level's L1 directory
+// (ones before each 65536-bit block) and its total
+__global__ void __launch_bounds__(1024) l1_scan_kernel(const u32* __restrict__ counts, u64 n_l1,
+                                                       u64* __restrict__ l1, u64* __restrict__ total) {
+  __shared__ u64 wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u64 per = (n_l1 + 1023) / 1024;
+  const u64 a = min(n_l1, (u64)tid * per), e = min(n_l1, a + per);
+  u64 s = 0;
+#pragma unroll 8
+  for (u64 i = a; i < e; ++i) s += __ldg(counts + i);
+  u64 inc = s;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u64 y = __shfl_up_sync(FULLM, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    u64 v = wsum[lane];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u64 y = __shfl_up_sync(FULLM, v, d);
+      if (lane >= d) v += y;
+    }
+    wsum[lane] = v;
+  }
+  __syncthreads();
+  u64 run = (warp ? wsum[warp - 1] : 0) + inc - s;
+#pragma unroll 8
+  for (u64 i = a; i < e; ++i) {
+    l1[i] = run;
+    run += __ldg(counts + i);
+  }
+  if (tid == 1023) *total = wsum[31];
+}
+
+namespace {
+template <typename TIn, typename TC, bool kLut>
+cudaError_t launch_w(const WLevelParams& p, int sms, cudaStream_t st) {
+  const size_t smem = 512 + (size_t)W_WARPS * WF<TIn, TC>::WARP_SMEM;
+  auto kern = wlevel_kernel<TIn, TC, kLut>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W_NT, smem);
+  if (per_sm < 1) per_sm = 1;
+  const u64 tiles = (p.m + WS<TIn>::TILE - 1) / WS<TIn>::TILE;
+  const u64 need = (tiles + W_WARPS - 1) / W_WARPS;
+  const u64 cap = (u64)sms * per_sm;
+  kern<<<(unsigned)(need < cap ? need : cap), W_NT, smem, st>>>(p);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_wlevel(const WLevelParams& p, int in_bytes, int code_bytes, bool lut, int sms,
+                          cudaStream_t st) {
+  if (p.m == 0) return cudaSuccess;
+  if (in_bytes == 1 && code_bytes == 1)
+    return lut ? launch_w<u8, u8, true>(p, sms, st) : launch_w<u8, u8, false>(p, sms, st);
+  if (in_bytes == 1 && code_bytes == 2) return launch_w<u8, u16, true>(p, sms, st);
+  if (in_bytes == 2 && code_bytes == 1) return launch_w<u16, u8, true>(p, sms, st);
+  if (in_bytes == 2 && code_bytes == 2)
+    return lut ? launch_w<u16, u16, true>(p, sms, st) : launch_w<u16, u16, false>(p, sms, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, const u16* lut, u32 shift_bit,
+                           u32* tile_counts, u32* l1_counts, int sms, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const u32 tiles = wlevel_tiles(n, in_bytes);
+  u64 blocks = (tiles + W_WARPS - 1) / W_WARPS;
+  if (blocks > (u64)sms * 8) blocks = (u64)sms * 8;
+  if (in_bytes == 1) {
+    if (lut)
+      wcount0_kernel<u8, true><<<(unsigned)blocks, W_NT, 0, st>>>((const u8*)text, n, lut, shift_bit, tile_counts, l1_counts);
+    else
+      wcount0_kernel<u8, false><<<(unsigned)blocks, W_NT, 0, st>>>((const u8*)text, n, lut, shift_bit, tile_counts, l1_counts);
+  } else {
+    if (lut)
+      wcount0_kernel<u16, true><<<(unsigned)blocks, W_NT, 0, st>>>((const u16*)text, n, lut, shift_bit, tile_counts, l1_counts);
+    else
+      wcount0_kernel<u16, false><<<(unsigned)blocks, W_NT, 0, st>>>((const u16*)text, n, lut, shift_bit, tile_counts, l1_counts);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_l1_scan(const u32* counts, u64 n_l1, u64* l1, u64* total, cudaStream_t st) {
+  l1_scan_kernel<<<1, 1024, 0, st>>>(counts, n_l1, l1, total);
+  return cudaGetLastError();
+}
+
+u32 wlevel_tiles(u64 m, int in_bytes) {
+  const u64 t = in_bytes == 1 ? WS<u8>::TILE : WS<u16>::TILE;
+  return (u32)((m + t - 1) / t);
+}
+
+}  // namespace wt

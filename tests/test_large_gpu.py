@@ -1,0 +1,89 @@
+"""GPU parity at sizes where every kernel path runs many tiles: full and
+partial tiles, single-node and multi-node tiles, LUT levels (level 0 through
+the symbol -> code map), u8 / u16 codes.  Every array of the device tree is
+compared with the oracle (the numpy restatement pinned to the reference's
+golden vectors), then batched queries are checked against the text."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from test_parity_gpu import assert_same_structure
+
+pytestmark = pytest.mark.gpu
+
+RNG = np.random.default_rng(20251017)
+
+
+def _zipf(n, sigma, a=1.2, seed=3):
+    r = np.random.default_rng(seed)
+    return (np.minimum(r.zipf(a, n), sigma) - 1).astype(np.uint16)
+
+
+LARGE = {
+    "u8_s256_full": lambda: np.random.default_rng(1).integers(0, 256, 1 << 22, dtype=np.uint8),
+    "u8_s256_partial": lambda: np.random.default_rng(2).integers(0, 256, (1 << 22) + 777,
+                                                                 dtype=np.uint8),
+    "u8_s200_lut": lambda: np.random.default_rng(3).integers(0, 200, (1 << 21) + 5,
+                                                             dtype=np.uint8),
+    "dna": lambda: np.frombuffer(b"ACGT", np.uint8)[
+        np.random.default_rng(4).integers(0, 4, (1 << 22) + 13)],
+    "u16_s4096": lambda: np.random.default_rng(5).integers(0, 4096, (1 << 21) + 3).astype(np.uint16),
+    "u16_zipf_inferred": lambda: _zipf((1 << 21) + 1, 65536),
+    "u8_skewed": lambda: np.minimum(np.random.default_rng(6).geometric(0.02, 1 << 21), 255)
+                            .astype(np.uint8),
+}
+
+
+@pytest.fixture(scope="module")
+def W():
+    import paper_2505_03372_b200 as w
+    return w
+
+
+def _check_queries(W, t, text, sigma_syms, m=20000, seed=9):
+    r = np.random.default_rng(seed)
+    n = len(text)
+    pos = r.integers(0, n, m)
+    assert np.array_equal(W.access_batch(t, pos), text[pos])
+    fa, fr, fs = O.text_answers(text, 1 << (8 * text.dtype.itemsize))
+    syms = sigma_syms[r.integers(0, len(sigma_syms), m)].astype(np.int64)
+    p = r.integers(0, n + 1, m)
+    assert np.array_equal(W.rank_batch(t, syms, p), fr(syms, p))
+    occ = {int(s): int(c) for s, c in zip(*np.unique(text, return_counts=True))}
+    present = np.array(sorted(occ), np.int64)
+    ss = present[r.integers(0, len(present), m)]
+    ks = 1 + (r.random(m) * np.array([occ[int(s)] for s in ss])).astype(np.int64)
+    assert np.array_equal(W.select_batch(t, ss, ks), fs(ss, ks))
+
+
+@pytest.mark.parametrize("name", sorted(LARGE))
+def test_large_build_and_queries(W, name):
+    text = LARGE[name]()
+    t = W.construct(text)
+    o = O.build(text)
+    assert_same_structure(t, o)
+    _check_queries(W, t, text, t.alphabet.sorted_symbols)
+
+
+def test_large_declared_alphabet_16_levels(W):
+    """C3z recipe at reduced n: Zipf over a declared 2^16 alphabet -> 16 full
+    levels with many multi-node tiles at the deep levels."""
+    text = _zipf(1 << 21, 65536, seed=11)
+    alpha = np.arange(65536, dtype=np.uint16)
+    t = W.construct_with_alphabet(text, alpha)
+    o = O.build_with_alphabet(text, alpha)
+    assert t.num_levels == 16
+    assert_same_structure(t, o)
+    _check_queries(W, t, text, alpha)
+
+
+def test_large_u8_text_u16_codes(W):
+    """u8 text with a declared 1000-symbol alphabet: level 0 reads bytes and
+    writes 16-bit codes (10 levels)."""
+    text = np.random.default_rng(12).integers(0, 256, (1 << 20) + 9, dtype=np.uint8)
+    alpha = np.arange(1000, dtype=np.uint16)
+    t = W.construct_with_alphabet(text, alpha)
+    o = O.build_with_alphabet(text, alpha)
+    assert t.num_levels == 10
+    assert_same_structure(t, o)

@@ -156,6 +156,11 @@ int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int64_t* args,
                   void* out, uint64_t m, uint64_t chunk, int flags, void* stream,
                   int64_t* bad_index, float* ms_out);
 
+/* Pinned host memory (cudaHostAlloc) for result arrays: device->host copies
+ * into it are asynchronous and overlap the next chunk's kernel.           */
+int wt_host_alloc(uint64_t bytes, void** out);
+int wt_host_free(void* p);
+
 /* Bit-vector query (WT_B_*) against one level of a built tree: the
  * RankSelectIndex methods of tree.rs[l] (rankselect.py:140-373).  Host
  * int64 arrays; callers validate ranges first.                             */

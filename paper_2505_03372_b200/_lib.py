@@ -10,6 +10,8 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
+import weakref
 
 import numpy as np
 
@@ -63,6 +65,8 @@ _SIGS = {
     "wt_tree_destroy": ([_vp], C.c_int),
     "wt_tree_query": ([_vp, _i32, _vp, _vp, _vp, _u64, _u64, _i32, _vp, C.POINTER(C.c_int64), _f32p], C.c_int),
     "wt_tree_level_query": ([_vp, _u32, _i32, _vp, _vp, _u64], C.c_int),
+    "wt_host_alloc": ([_u64, C.POINTER(_vp)], C.c_int),
+    "wt_host_free": ([_vp], C.c_int),
     "wt_nccl_unique_id": ([_vp], C.c_int),
     "wt_tree_replicate": ([_vp, _vp, _i32, _i32, _i32, C.POINTER(_vp), _f32p], C.c_int),
     "wt_bits_build": ([_vp, _u64, _i32, _u32, _u64, _i32, C.POINTER(_vp)], C.c_int),
@@ -99,3 +103,39 @@ def ptr(a: np.ndarray | None):
 
 def current_device() -> int:
     return int(os.environ.get("WT_DEVICE", "0"))
+
+
+# ---------------------------------------------------------------------------
+# pinned result arrays: device -> host copies into page-locked memory are
+# asynchronous (the query pipeline overlaps them with the next chunk's
+# kernel).  Blocks are cached by size and return to the cache when the last
+# numpy view of them is dropped.
+# ---------------------------------------------------------------------------
+PINNED_MIN_BYTES = 1 << 20
+_pin_lock = threading.Lock()
+_pin_free: dict[int, list[int]] = {}
+
+
+def _pin_release(nbytes: int, addr: int) -> None:
+    with _pin_lock:
+        _pin_free.setdefault(nbytes, []).append(addr)
+
+
+def pinned_empty(count: int, dtype) -> np.ndarray:
+    """An uninitialised array in pinned host memory (plain np.empty below
+    PINNED_MIN_BYTES, or when page-locked memory cannot be had)."""
+    dtype = np.dtype(dtype)
+    nbytes = int(count) * dtype.itemsize
+    if nbytes < PINNED_MIN_BYTES:
+        return np.empty(count, dtype)
+    with _pin_lock:
+        free = _pin_free.get(nbytes)
+        addr = free.pop() if free else None
+    if addr is None:
+        p = C.c_void_p()
+        if lib.wt_host_alloc(nbytes, C.byref(p)) != WT_OK or not p.value:
+            return np.empty(count, dtype)
+        addr = p.value
+    holder = (C.c_uint8 * nbytes).from_address(addr)
+    weakref.finalize(holder, _pin_release, nbytes, addr)
+    return np.frombuffer(holder, dtype, count)

@@ -237,7 +237,8 @@ struct wt_tree {
   // query staging (reused across calls)
   void* qbuf[2] = {nullptr, nullptr};
   size_t qbuf_bytes = 0;
-  cudaStream_t qstream[2] = {nullptr, nullptr};
+  cudaStream_t qstream[3] = {nullptr, nullptr, nullptr};  // copy-in, compute, copy-out
+  cudaEvent_t qev[3][2] = {};                              // per stage and slot
   std::mutex qmutex;
   // build profile: [0] text upload + histogram + plan, [1 + l] level-l kernel (ms)
   std::vector<float> build_ms;
@@ -409,6 +410,9 @@ static void free_tree_arrays(wt_tree* t) {
   F(t->qbuf[1]);
   for (auto& s : t->qstream)
     if (s) cudaStreamDestroy(s);
+  for (auto& a : t->qev)
+    for (auto& e : a)
+      if (e) cudaEventDestroy(e);
   if (t->stream) cudaStreamDestroy(t->stream);
 }
 
@@ -920,13 +924,20 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
     }
     return WT_OK;
   }
-  // host buffers: chunked, double-buffered over two streams (
-  // batch.py:152-239 keeps at most two chunks staged)
+  // host buffers: a 3-stage pipeline over two device chunk slots -- the
+  // copy-in of chunk c+1, the kernel of chunk c and the copy-out of chunk c-1
+  // run on three streams at once (batch.py:152-239 keeps at
+  // most two chunks staged).  Copies are only asynchronous from pinned host
+  // memory (the Python layer hands pinned result arrays for large batches).
   if (chunk == 0) chunk = 1ull << 22;
   if (chunk > m) chunk = m;
   const size_t need = chunk * (16 + out_elem) + 64;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 3; ++i) {
     if (!t->qstream[i]) CU(cudaStreamCreateWithFlags(&t->qstream[i], cudaStreamNonBlocking));
+    for (int j = 0; j < 2; ++j)
+      if (!t->qev[i][j]) CU(cudaEventCreateWithFlags(&t->qev[i][j], cudaEventDisableTiming));
+  }
+  for (int i = 0; i < 2; ++i) {
     if (t->qbuf_bytes < need && t->qbuf[i]) {
       CU(cudaFree(t->qbuf[i]));
       t->qbuf[i] = nullptr;
@@ -934,65 +945,82 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
     if (!t->qbuf[i]) CU(cudaMalloc(&t->qbuf[i], need));
   }
   t->qbuf_bytes = std::max(t->qbuf_bytes, need);
-  if (validate) CU(cudaMemset(t->bad, 0xff, 8));
-  cudaEvent_t ev[2][2];
-  for (auto& a : ev)
-    for (auto& e : a) CU(cudaEventCreate(&e));
-  float total_ms = 0.f;
-  int rc = WT_OK;
+  cudaStream_t sin = t->qstream[0], sk = t->qstream[1], sout = t->qstream[2];
+  if (validate) {
+    CU(cudaMemsetAsync(t->bad, 0xff, 8, sk));
+  }
   const uint64_t nchunks = (m + chunk - 1) / chunk;
+  std::vector<cudaEvent_t> kt;  // kernel timing events (ms_out)
+  if (ms_out) {
+    kt.resize(2 * nchunks);
+    for (auto& e : kt) CU(cudaEventCreate(&e));
+  }
+  int rc = WT_OK;
   for (uint64_t c = 0; c < nchunks && rc == WT_OK; ++c) {
     const int s = (int)(c & 1);
-    cudaStream_t st = t->qstream[s];
-    if (c >= 2 && ms_out) {  // harvest the timing of the chunk that used this slot
-      float ms = 0;
-      if (cudaEventSynchronize(ev[s][1]) == cudaSuccess &&
-          cudaEventElapsedTime(&ms, ev[s][0], ev[s][1]) == cudaSuccess)
-        total_ms += ms;
-    }
     const uint64_t a = c * chunk, cnt = std::min(chunk, m - a);
     u8* base = (u8*)t->qbuf[s];
     i64* d_ids = (i64*)base;
     i64* d_args = (i64*)(base + chunk * 8);
     u8* d_out = base + chunk * 16;
-    if (kind != WT_Q_ACCESS &&
-        cudaMemcpyAsync(d_ids, ids + a, cnt * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
-      rc = fail(WT_ERR_CUDA, "H2D ids");
-    if (rc == WT_OK &&
-        cudaMemcpyAsync(d_args, args + a, cnt * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
-      rc = fail(WT_ERR_CUDA, "H2D args");
-    if (rc != WT_OK) break;
-    cudaEventRecord(ev[s][0], st);
-    cudaError_t e = launch_query(t->dev, kind, out_kind, validate, d_ids, d_args, d_out, cnt,
-                                 t->rate_log, a, t->bad, st);
-    if (e != cudaSuccess) {
-      rc = fail(WT_ERR_CUDA, std::string("query kernel: ") + cudaGetErrorString(e));
-      break;
-    }
-    cudaEventRecord(ev[s][1], st);
-    if (cudaMemcpyAsync((u8*)out + a * out_elem, d_out, cnt * out_elem, cudaMemcpyDeviceToHost,
-                        st) != cudaSuccess)
-      rc = fail(WT_ERR_CUDA, "D2H out");
+    cudaError_t e = cudaSuccess;
+    // copy-in: slot s is free once the kernel of chunk c-2 has read it
+    if (c >= 2) e = cudaStreamWaitEvent(sin, t->qev[1][s], 0);
+    if (e == cudaSuccess && kind != WT_Q_ACCESS)
+      e = cudaMemcpyAsync(d_ids, ids + a, cnt * 8, cudaMemcpyHostToDevice, sin);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_args, args + a, cnt * 8, cudaMemcpyHostToDevice, sin);
+    if (e == cudaSuccess) e = cudaEventRecord(t->qev[0][s], sin);
+    // kernel: inputs landed, and the copy-out of chunk c-2 has drained d_out
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sk, t->qev[0][s], 0);
+    if (e == cudaSuccess && c >= 2) e = cudaStreamWaitEvent(sk, t->qev[2][s], 0);
+    if (e == cudaSuccess && ms_out) e = cudaEventRecord(kt[2 * c], sk);
+    if (e == cudaSuccess)
+      e = launch_query(t->dev, kind, out_kind, validate, d_ids, d_args, d_out, cnt, t->rate_log, a,
+                       t->bad, sk);
+    if (e == cudaSuccess && ms_out) e = cudaEventRecord(kt[2 * c + 1], sk);
+    if (e == cudaSuccess) e = cudaEventRecord(t->qev[1][s], sk);
+    // copy-out
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, t->qev[1][s], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync((u8*)out + a * out_elem, d_out, cnt * out_elem, cudaMemcpyDeviceToHost, sout);
+    if (e == cudaSuccess) e = cudaEventRecord(t->qev[2][s], sout);
+    if (e != cudaSuccess) rc = fail(WT_ERR_CUDA, std::string("query pipeline: ") + cudaGetErrorString(e));
   }
-  for (int s = 0; s < 2; ++s) {
-    cudaError_t e = cudaStreamSynchronize(t->qstream[s]);
+  for (int i = 0; i < 3; ++i) {
+    cudaError_t e = cudaStreamSynchronize(t->qstream[i]);
     if (e != cudaSuccess && rc == WT_OK) rc = fail(WT_ERR_CUDA, cudaGetErrorString(e));
   }
   if (ms_out && rc == WT_OK) {
-    for (uint64_t c = nchunks >= 2 ? nchunks - 2 : 0; c < nchunks; ++c) {
+    float total_ms = 0.f;
+    for (uint64_t c = 0; c < nchunks; ++c) {
       float ms = 0;
-      const int s = (int)(c & 1);
-      if (cudaEventElapsedTime(&ms, ev[s][0], ev[s][1]) == cudaSuccess) total_ms += ms;
+      if (cudaEventElapsedTime(&ms, kt[2 * c], kt[2 * c + 1]) == cudaSuccess) total_ms += ms;
     }
     *ms_out = total_ms;
   }
-  for (auto& a : ev)
-    for (auto& e : a) cudaEventDestroy(e);
+  for (auto& e : kt) cudaEventDestroy(e);
   if (rc == WT_OK && validate && bad_index) {
     cudaError_t e = cudaMemcpy(bad_index, t->bad, 8, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) rc = fail(WT_ERR_CUDA, cudaGetErrorString(e));
   }
   return rc;
+}
+
+// pinned host memory for result arrays (so the copy-out is asynchronous)
+extern "C" int wt_host_alloc(uint64_t bytes, void** out) {
+  if (!out) return fail(WT_ERR_ARG, "NULL out");
+  *out = nullptr;
+  if (!bytes) return WT_OK;
+  if (cudaHostAlloc(out, bytes, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    *out = nullptr;
+    return fail(WT_ERR_OOM, "cudaHostAlloc failed");
+  }
+  return WT_OK;
+}
+extern "C" int wt_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+  return WT_OK;
 }
 
 // per-level bit-vector queries on a built tree (RankSelectIndex methods of

@@ -182,11 +182,11 @@ class WaveletTree:
         args = np.ascontiguousarray(np.asarray(args, np.int64).reshape(-1))
         m = len(args)
         if kind == _lib.Q_ACCESS:
-            out = np.empty(m, np.int64 if access_ids else self.alphabet.sorted_symbols.dtype)
+            out = _lib.pinned_empty(m, np.int64 if access_ids else self.alphabet.sorted_symbols.dtype)
             ids_a = None
         else:
             ids_a = np.ascontiguousarray(np.asarray(ids, np.int64).reshape(-1))
-            out = np.empty(m, np.int64)
+            out = _lib.pinned_empty(m, np.int64)
         if m == 0:
             return out, -1
         flags = (_lib.F_SYMBOLS if symbols else 0) | (_lib.F_ACCESS_IDS if access_ids else 0)

@@ -22,7 +22,7 @@ __global__ void walk(const ulonglong2* __restrict__ lines, uint64_t n_lines, uin
   uint64_t acc = 0;
   for (int s = 0; s < steps; ++s) {
     x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 29;
-    const uint64_t li = (x + acc) % n_lines;  // dependent on the previous line
+    const uint64_t li = (x + acc) & (n_lines - 1);  // dependent on the previous line
     const ulonglong2* L = lines + li * 4;
     const ulonglong2 a = ld_line16(L), b = ld_line16(L + 1), c = ld_line16(L + 2), d = ld_line16(L + 3);
     acc += (a.x ^ b.y ^ c.x ^ d.y) & 1;
@@ -37,7 +37,7 @@ __global__ void copyk(const uint4* __restrict__ a, uint4* __restrict__ b, uint64
 }
 
 int main() {
-  const uint64_t bytes = 3ull << 30;  // 3 GiB table (>> 126 MB L2)
+  const uint64_t bytes = 2ull << 30;  // 2 GiB table (>> 126 MB L2), power of two lines
   const uint64_t n_lines = bytes / 64;
   ulonglong2* lines;
   uint64_t* out;

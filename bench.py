@@ -201,21 +201,9 @@ def run_ours(args):
     # ---------------- replicate over NCCL --------------------------------------
     replicate = None
     if world > 1:
-        uid = (C.c_uint8 * 128)()
-        if rank == 0:
-            _lib.check(_lib.lib.wt_nccl_unique_id(uid), "wt_nccl_unique_id")
-        obj = [bytes(uid)] if rank == 0 else [None]
-        dist.broadcast_object_list(obj, src=0)
-        uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
-        out = C.c_void_p()
-        rms = C.c_float(0)
-        _lib.check(_lib.lib.wt_tree_replicate(tree.handle if rank == 0 else None, uid, rank,
-                                              world, local, C.byref(out), C.byref(rms)),
-                   "wt_tree_replicate")
-        if rank != 0:
-            from paper_2505_03372_b200.wtree import WaveletTree, _TreeHandle
-            tree = WaveletTree(_TreeHandle(out), 1, np.uint8)
-        replicate = {"ms": max_over_ranks(float(rms.value)),
+        from paper_2505_03372_b200 import parallel as par
+        tree = par.replicate(tree if rank == 0 else None, device=local)
+        replicate = {"ms": max_over_ranks(float(tree.replicate_ms)),
                      "bytes": int(tree.device_bytes)}
         replicate["GB_per_s"] = replicate["bytes"] / (replicate["ms"] / 1e3) / 1e9
 

@@ -619,7 +619,14 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       }
       if (P.L && P.sizes[0]) {
         CU(cudaMemsetAsync(l1cnt[0], 0, (t->lv[0].meta.n_l1 + 4) * 4, st));
-        CU(launch_wcount0(dtext, n, sym_bytes, dlut, P.L - 1, tcnt[0], l1cnt[0], sm_count(device), st));
+        // level-0 bit = top code bit = (symbol >= thr): codes are monotone in the symbol
+        uint32_t thr = 0x10000u;
+        for (uint32_t i = 0; i < P.sigma; ++i)
+          if ((P.values[i] >> (P.L - 1)) & 1u) {
+            thr = P.symbols[i];
+            break;
+          }
+        CU(launch_wcount0(dtext, n, sym_bytes, thr, tcnt[0], l1cnt[0], sm_count(device), st));
       }
       int ci = 0;
       for (uint32_t l = 0; l < P.L; ++l) {

@@ -62,8 +62,9 @@ struct WLevelParams {
 cudaError_t launch_wlevel(const WLevelParams& p, int in_bytes, int code_bytes, bool lut, int sms,
                           cudaStream_t st);
 u32 wlevel_tiles(u64 m, int in_bytes);
-cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, const u16* lut, u32 shift_bit,
-                           u32* tile_counts, u32* l1_counts, int sms, cudaStream_t st);
+// ones per warp tile of level 0: text symbols >= thr (the top code bit)
+cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, u32 thr, u32* tile_counts,
+                           u32* l1_counts, int sms, cudaStream_t st);
 // exclusive scan of per-L1-block counts -> l1[0..n_l1) and the level total
 cudaError_t launch_l1_scan(const u32* counts, u64 n_l1, u64* l1, u64* total, cudaStream_t st);
 

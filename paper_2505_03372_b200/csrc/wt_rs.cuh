@@ -120,14 +120,18 @@ __device__ __forceinline__ u32 ld_u32_64b(const u32* p) {
   return v;
 }
 
+// one 64-byte line as two 256-bit loads (LDG.256, sm_100): half the LSU
+// instructions of 16-byte loads, which kept the query kernels lg-throttled
+__device__ __forceinline__ void ld_line32(const ulonglong2* p, u64& a, u64& b, u64& c, u64& d) {
+  asm volatile("ld.global.nc.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+               : "l"(p));
+}
 __device__ __forceinline__ QLine qload(const QLevelDev& Q, u64 i) {
   const ulonglong2* L = Q.lines + i * 4;
-  const ulonglong2 a = ld_line16(L), b = ld_line16(L + 1), c = ld_line16(L + 2),
-                   d = ld_line16(L + 3);
   QLine r;
-  r.hdr = a.x;
-  r.wd[0] = a.y; r.wd[1] = b.x; r.wd[2] = b.y; r.wd[3] = c.x; r.wd[4] = c.y; r.wd[5] = d.x;
-  r.wd[6] = d.y;
+  ld_line32(L, r.hdr, r.wd[0], r.wd[1], r.wd[2]);
+  ld_line32(L + 2, r.wd[3], r.wd[4], r.wd[5], r.wd[6]);
   return r;
 }
 
@@ -181,22 +185,22 @@ __device__ __forceinline__ u64 qselect(const QLevelDev& Q, u64 k) {
   }
   const QLine L = qload(Q, lo);
   k -= kOnes ? L.hdr : lo * kQBits - L.hdr;
-  u64 res = lo * kQBits;
+  // find the word first (predicated selects), then ONE in-word select: inside
+  // the loop it would run once per distinct word index in the warp
+  u32 wi = 6, kk = (u32)k;
+  u64 ws = kOnes ? L.wd[6] : ~L.wd[6];
   bool done = false;
 #pragma unroll
-  for (int x = 0; x < 7; ++x) {
+  for (int x = 0; x < 6; ++x) {
     const u64 word = kOnes ? L.wd[x] : ~L.wd[x];
     const u32 pc = __popcll(word);
-    if (!done) {
-      if (pc >= k) {
-        res += 64 * x + select_in_word64(word, (u32)k);
-        done = true;
-      } else {
-        k -= pc;
-      }
-    }
+    const bool here = !done && pc >= kk;
+    wi = here ? (u32)x : wi;
+    ws = here ? word : ws;
+    kk -= (!done && !here) ? pc : 0u;
+    done = done || here;
   }
-  return res;
+  return lo * kQBits + 64 * wi + select_in_word64(ws, kk);
 }
 
 }  // namespace wt

@@ -748,23 +748,125 @@ __global__ void __launch_bounds__(W_NT) wlevel_kernel(const __grid_constant__ WL
 }
 
 // ---------------------------------------------------------------------------
+// the last level (nothing to partition): bits, L2 entries and samples only.
+// Lane i owns input bytes [64i, 64i + 64) of a warp tile, so its mask is one
+// contiguous 64-bit (u8 codes) / 32-bit (u16 codes) piece of the bit-vector
+// and a single warp scan gives every L2 prefix.
+// ---------------------------------------------------------------------------
+template <typename TIn, typename TC, bool kLut>
+__global__ void __launch_bounds__(256) wlast_kernel(const __grid_constant__ WLevelParams P) {
+  using S = WS<TIn>;
+  constexpr int TILE = S::TILE, TPL1 = S::TPL1;
+  constexpr int CH = 16 / (int)sizeof(TIn);   // elements per 16-byte chunk
+  constexpr int E = 4 * CH;                   // elements per lane (64 | 32)
+  constexpr int WPC = CH * (int)sizeof(TC) / 4;
+  __shared__ u16 slut[kLut && sizeof(TIn) == 1 ? 256 : 1];
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (kLut && sizeof(TIn) == 1) {
+    for (int i = tid; i < 256; i += 256) slut[i] = P.lut[i];
+    __syncthreads();
+  }
+  const u32 ntiles = (u32)((P.m + TILE - 1) / TILE);
+  const u32 nw = gridDim.x * 8;
+  const u8* in = reinterpret_cast<const u8*>(P.in);
+  const u64 l2m = (1ull << P.l2_log) - 1;
+  for (u32 t = blockIdx.x * 8 + (tid >> 5); t < ntiles; t += nw) {
+    const u64 t0 = (u64)t * TILE;
+    const u32 valid = (u32)min((u64)TILE, P.m - t0);
+    // P1 loads first (independent of the data)
+    const u32 b = t / TPL1, tb = t - b * TPL1;
+    u32 pre = 0;
+#pragma unroll
+    for (int r = 0; r < TPL1 / 32; ++r) {
+      const u32 j = r * 32 + lane;
+      if (j < tb) pre += __ldg(P.tile_counts + b * TPL1 + j);
+    }
+    const u64 l1v = __ldg(P.l1 + b);
+    const u8* base = in + t0 * sizeof(TIn) + lane * 64;
+    const u32 e0 = (u32)lane * E;  // first element of this lane in the tile
+    u64 m = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const u32 e = e0 + k * CH;
+      uint4 q;
+      if (e + CH <= valid) {
+        q = __ldg(reinterpret_cast<const uint4*>(base + k * 16));
+      } else {
+        u32 w[4] = {0, 0, 0, 0};
+        for (u32 bb = 0; bb < 16 && e * sizeof(TIn) + bb < valid * sizeof(TIn); ++bb)
+          w[bb >> 2] |= (u32)base[k * 16 + bb] << (8 * (bb & 3));
+        q = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      u32 cw[WPC];
+      wcodes<TIn, TC, kLut, WPC>(q, slut, P.lut, cw);
+      u32 mk = wmask<TC, WPC>(cw, P.shift_bit);
+      if (e + CH > valid) mk &= e >= valid ? 0u : (1u << (valid - e)) - 1u;
+      m |= (u64)mk << (k * CH);
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) pre += __shfl_xor_sync(FULLM, pre, d);
+    const u64 P1 = l1v + pre;
+    const u32 c = __popcll(m);
+    u32 inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 y = __shfl_up_sync(FULLM, inc, d);
+      if (lane >= d) inc += y;
+    }
+    const u32 tile_ones = __shfl_sync(FULLM, inc, 31);
+    const u32 pl = inc - c;  // ones of the tile before this lane
+    if (e0 < ((valid + 63u) & ~63u)) {
+      if (E == 64)
+        P.words[(t0 >> 6) + lane] = m;
+      else
+        reinterpret_cast<u32*>(P.words)[(t0 >> 5) + lane] = (u32)m;
+    }
+    const u64 g = t0 + e0;
+    if (e0 < valid && (g & l2m) == 0) P.l2[g >> P.l2_log] = (u16)(P1 + pl - l1v);
+    // select samples (rankselect.py:509-532)
+    const u32 lv = e0 >= valid ? 0u : min((u32)E, valid - e0);
+    const u64 vmask = lv >= 64 ? ~0ull : ((1ull << lv) - 1);
+#pragma unroll
+    for (int kind = 0; kind < 2; ++kind) {
+      const bool ones = kind == 0;
+      const u64 sb = ones ? P1 : t0 - P1;
+      const u32 cnt = ones ? tile_ones : valid - tile_ones;
+      const u64 q0 = wnext_multiple(sb, P.rate, P.rate_log);
+      if (q0 > sb + cnt) continue;
+      const u64 mk = ones ? m : (~m & vmask);
+      const u32 lp = ones ? pl : e0 - pl;
+      const u32 lc = __popcll(mk);
+      u64* out = ones ? P.ones : P.zeros;
+      const u64 cap = ones ? P.ones_cap : P.zeros_cap;
+      for (u64 qo = q0; qo <= sb + cnt; qo += P.rate) {
+        const u32 tt = (u32)(qo - sb);
+        if (lp < tt && tt <= lp + lc) {
+          const u64 sidx = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
+          if (sidx < cap) out[sidx] = g + select_in_word64(mk, tt - lp);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // level 0: ones per warp tile of the text's top code bit (streaming pass)
 // ---------------------------------------------------------------------------
-template <typename TIn, bool kLut>
-__global__ void __launch_bounds__(W_NT) wcount0_kernel(const TIn* __restrict__ text, u64 n,
-                                                      const u16* __restrict__ lut, u32 shift_bit,
+// Codes are monotone in the symbol (the minimal alphabet and the reduced-tree
+// codes both preserve order, alphabet.py:94-111, :160-207), so the top code
+// bit of a text symbol is simply `symbol >= thr`, thr = the smallest symbol
+// whose code has it set: a SWAR byte / halfword compare, no LUT.
+template <typename TIn>
+__global__ void __launch_bounds__(256) wcount0_kernel(const TIn* __restrict__ text, u64 n, u32 thr,
                                                       u32* __restrict__ tile_counts,
                                                       u32* __restrict__ l1_counts) {
   using S = WS<TIn>;
   constexpr int CH = S::CH;
-  __shared__ u16 slut[kLut && sizeof(TIn) == 1 ? 256 : 1];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (kLut && sizeof(TIn) == 1) {
-    for (int i = tid; i < 256; i += W_NT) slut[i] = lut[i];
-    __syncthreads();
-  }
+  const int lane = threadIdx.x & 31;
   const u32 ntiles = (u32)((n + S::TILE - 1) / S::TILE);
-  for (u32 t = blockIdx.x * W_WARPS + warp; t < ntiles; t += gridDim.x * W_WARPS) {
+  const u32 t4 = sizeof(TIn) == 1 ? thr * 0x01010101u : thr * 0x00010001u;
+  const bool none = thr > (sizeof(TIn) == 1 ? 0xffu : 0xffffu);
+  for (u32 t = blockIdx.x * 8 + (threadIdx.x >> 5); t < ntiles; t += gridDim.x * 8) {
     uint4 q[W_K];
     wload<TIn>(reinterpret_cast<const u8*>(text), n, t, lane, q);
     const u64 t0 = (u64)t * S::TILE;
@@ -772,15 +874,21 @@ __global__ void __launch_bounds__(W_NT) wcount0_kernel(const TIn* __restrict__ t
 #pragma unroll
     for (int k = 0; k < W_K; ++k) {
       const u32 e = (u32)(k * 32 + lane) * CH;
-      const u32 qw[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+      const u32 w4[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+      u32 c = 0;
 #pragma unroll
-      for (int j = 0; j < CH; ++j) {
-        if (t0 + e + j >= n) break;
-        const u32 raw = sizeof(TIn) == 1 ? (qw[j >> 2] >> ((j & 3) * 8)) & 0xffu
-                                         : (qw[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
-        const u32 code = !kLut ? raw : sizeof(TIn) == 1 ? (u32)slut[raw] : (u32)__ldg(lut + raw);
-        cnt += (code >> shift_bit) & 1u;
+      for (int i = 0; i < 4; ++i)
+        c += sizeof(TIn) == 1 ? __popc(__vcmpgeu4(w4[i], t4)) >> 3
+                              : __popc(__vcmpgeu2(w4[i], t4)) >> 4;
+      if (t0 + e + CH > n) {  // tail: zero-filled bytes may compare >= thr only if thr == 0
+        c = 0;
+        for (int j = 0; j < CH && t0 + e + j < n; ++j) {
+          const u32 raw = sizeof(TIn) == 1 ? (w4[j >> 2] >> ((j & 3) * 8)) & 0xffu
+                                           : (w4[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+          c += raw >= thr;
+        }
       }
+      cnt += none ? 0u : c;
     }
 #pragma unroll
     for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(FULLM, cnt, d);
@@ -840,6 +948,12 @@ cudaError_t launch_w(const WLevelParams& p, int sms, cudaStream_t st) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W_NT, smem);
   if (per_sm < 1) per_sm = 1;
   const u64 tiles = (p.m + WS<TIn>::TILE - 1) / WS<TIn>::TILE;
+  if (!p.out) {  // the last level: no partition
+    u64 blocks = (tiles + 7) / 8;
+    if (blocks > (u64)sms * 8) blocks = (u64)sms * 8;
+    wlast_kernel<TIn, TC, kLut><<<(unsigned)blocks, 256, 0, st>>>(p);
+    return cudaGetLastError();
+  }
   const u64 need = (tiles + W_WARPS - 1) / W_WARPS;
   const u64 cap = (u64)sms * per_sm;
   kern<<<(unsigned)(need < cap ? need : cap), W_NT, smem, st>>>(p);
@@ -859,23 +973,16 @@ cudaError_t launch_wlevel(const WLevelParams& p, int in_bytes, int code_bytes, b
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, const u16* lut, u32 shift_bit,
-                           u32* tile_counts, u32* l1_counts, int sms, cudaStream_t st) {
+cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, u32 thr, u32* tile_counts,
+                           u32* l1_counts, int sms, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const u32 tiles = wlevel_tiles(n, in_bytes);
-  u64 blocks = (tiles + W_WARPS - 1) / W_WARPS;
-  if (blocks > (u64)sms * 8) blocks = (u64)sms * 8;
-  if (in_bytes == 1) {
-    if (lut)
-      wcount0_kernel<u8, true><<<(unsigned)blocks, W_NT, 0, st>>>((const u8*)text, n, lut, shift_bit, tile_counts, l1_counts);
-    else
-      wcount0_kernel<u8, false><<<(unsigned)blocks, W_NT, 0, st>>>((const u8*)text, n, lut, shift_bit, tile_counts, l1_counts);
-  } else {
-    if (lut)
-      wcount0_kernel<u16, true><<<(unsigned)blocks, W_NT, 0, st>>>((const u16*)text, n, lut, shift_bit, tile_counts, l1_counts);
-    else
-      wcount0_kernel<u16, false><<<(unsigned)blocks, W_NT, 0, st>>>((const u16*)text, n, lut, shift_bit, tile_counts, l1_counts);
-  }
+  u64 blocks = (tiles + 7) / 8;
+  if (blocks > (u64)sms * 16) blocks = (u64)sms * 16;
+  if (in_bytes == 1)
+    wcount0_kernel<u8><<<(unsigned)blocks, 256, 0, st>>>((const u8*)text, n, thr, tile_counts, l1_counts);
+  else
+    wcount0_kernel<u16><<<(unsigned)blocks, 256, 0, st>>>((const u16*)text, n, thr, tile_counts, l1_counts);
   return cudaGetLastError();
 }
 

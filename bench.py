@@ -239,15 +239,21 @@ def run_ours(args):
     sptr = C.c_void_p(stream.cuda_stream)
     bad = C.c_int64(-1)
     flags = _lib.F_DEVICE_PTRS | _lib.F_SYMBOLS
+    # device sort_queries_by_symbol (WT_F_SORT, the paper's query sorting) pays
+    # for access and select; rank runs unsorted (measured: sorting costs more
+    # than it saves there).  The sort runs inside the timed region.
+    sort_kinds = set() if args.no_sort else {"access", "select"}
     h = tree.handle
     batches = [("access", _lib.Q_ACCESS, None, q_acc, o_acc),
                ("rank", _lib.Q_RANK, q_rsym, q_rpos, o_rank),
                ("select", _lib.Q_SELECT, q_ssym, q_ks, o_sel)]
+    kind_name = {b[1]: b[0] for b in batches}
 
     def launch(kind, ids, a, o):
+        fl = flags | (_lib.F_SORT if kind_name[kind] in sort_kinds else 0)
         _lib.check(_lib.lib.wt_tree_query(h, kind, C.c_void_p(ids.data_ptr()) if ids is not None
                                           else None, C.c_void_p(a.data_ptr()),
-                                          C.c_void_p(o.data_ptr()), a.numel(), 0, flags, sptr,
+                                          C.c_void_p(o.data_ptr()), a.numel(), 0, fl, sptr,
                                           C.byref(bad), None), "query")
         if bad.value != -1:
             raise RuntimeError(f"invalid query {bad.value}")
@@ -299,15 +305,15 @@ def run_ours(args):
         h_acc, h_rsym, h_rpos, h_ssym, h_ks = map(pin, (q_acc, q_rsym, q_rpos, q_ssym, q_ks))
         chunk = 1 << 22  # 8 chunks per kind: the copy-in / kernel / copy-out pipeline overlaps
         for _ in range(max(2, args.warmup)):  # also fills the pinned result-array cache
-            ra = W.access_batch(tree, h_acc, chunk_size=chunk)
-            rr = W.rank_batch(tree, h_rsym, h_rpos, chunk_size=chunk)
-            rs = W.select_batch(tree, h_ssym, h_ks, chunk_size=chunk)
+            ra = W.access_batch(tree, h_acc, chunk_size=chunk, sort="access" in sort_kinds)
+            rr = W.rank_batch(tree, h_rsym, h_rpos, chunk_size=chunk, sort="rank" in sort_kinds)
+            rs = W.select_batch(tree, h_ssym, h_ks, chunk_size=chunk, sort="select" in sort_kinds)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            ra = W.access_batch(tree, h_acc, chunk_size=chunk)
-            rr = W.rank_batch(tree, h_rsym, h_rpos, chunk_size=chunk)
-            rs = W.select_batch(tree, h_ssym, h_ks, chunk_size=chunk)
+            ra = W.access_batch(tree, h_acc, chunk_size=chunk, sort="access" in sort_kinds)
+            rr = W.rank_batch(tree, h_rsym, h_rpos, chunk_size=chunk, sort="rank" in sort_kinds)
+            rs = W.select_batch(tree, h_ssym, h_ks, chunk_size=chunk, sort="select" in sort_kinds)
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / args.steps)
         assert np.array_equal(ra, o_acc.cpu().numpy()) and np.array_equal(rr, o_rank.cpu().numpy())
@@ -332,7 +338,8 @@ def run_ours(args):
                                       "query recipe generated on device)",
             "config": {"workload": "C2/C5: n=2^%d u8 text, sigma=256; %d mixed "
                                    "access/rank/select queries per GPU per step "
-                                   "(equal thirds, kind-homogeneous batches)"
+                                   "(equal thirds, kind-homogeneous batches; access and select "
+                                   "sorted on the device by symbol / position first)"
                                    % (args.n_log, m_total),
                        "n": n, "sigma": sigma, "queries_per_gpu": m_total,
                        "parallelism": f"replicas x{world} (NCCL broadcast)",
@@ -340,7 +347,7 @@ def run_ours(args):
                              % (tree.device_bytes / 1e9, m_total * 16 / 1e9)},
             "queries": queries, "build": build, "replicate": replicate,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": args.steps * sum(4 if b[0] in sort_kinds else 1 for b in batches),
             "clocks": clk.summary(),
         }
         print(json.dumps(line))
@@ -490,6 +497,7 @@ def main():
     ap.add_argument("--queries", type=int, default=100_000_000)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sort", action="store_true", help="no device query sorting")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--ref-n-log", type=int, default=24)
     ap.add_argument("--ref-queries-per-proc", type=int, default=40000)

@@ -30,7 +30,7 @@ lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
 WT_OK, WT_ERR_CUDA, WT_ERR_ARG, WT_ERR_OOM, WT_ERR_SYMBOL, WT_ERR_NCCL, WT_ERR_BUILD = range(7)
 Q_ACCESS, Q_RANK, Q_SELECT = 0, 1, 2
 B_RANK1, B_RANK0, B_SELECT1, B_SELECT0, B_BIT = range(5)
-F_DEVICE_PTRS, F_SYMBOLS, F_ACCESS_IDS = 1, 2, 4
+F_DEVICE_PTRS, F_SYMBOLS, F_ACCESS_IDS, F_SORT = 1, 2, 4, 8
 (A_SYMBOLS, A_CODE_VALUES, A_CODE_LENS, A_CUM_HIST, A_LEVEL_SIZES, A_REGION_OFFS, A_WORDS,
  A_L1, A_L2, A_ONES, A_ZEROS, A_NODE_STARTS, A_NODE_RANK0) = range(13)
 

@@ -71,10 +71,14 @@ class BatchRunner:
     """Runs batches against one device tree; one in-flight batch per runner."""
 
     def __init__(self, tree: WaveletTree, chunk_size: int = DEFAULT_CHUNK_SIZE,
-                 workers: int = 1):
+                 workers: int = 1, *, sort: bool = False):
+        """``sort=True`` (extension): each chunk is sorted on the device by
+        symbol and coarse position before the walk (the paper's query sorting,
+        PAPER.md:928, :988); results stay in query order."""
         if chunk_size < 1:
             raise ValueError("chunk_size must be positive")
         self.tree = tree
+        self.sort = bool(sort)
         self.chunk_size = chunk_size
         self.workers = max(1, int(workers))
         self.staging_allocated_records = 0
@@ -115,30 +119,31 @@ class BatchRunner:
         t0 = time.perf_counter()
         syms = None if batch.kind == "access" else batch.symbols
         out, bad = tree.query(_KIND_ID[batch.kind], syms, batch.args, symbols=True,
-                              chunk=chunk)
+                              chunk=chunk, sort=self.sort)
         self.process_seconds = time.perf_counter() - t0
         if bad >= 0:
             raise BatchError(bad, self._cause(batch, bad))
         return out
 
 
-def run_batch(tree: WaveletTree, batch: QueryBatch, workers: int = 1) -> np.ndarray:
-    return BatchRunner(tree, batch.chunk_size, workers).run(batch)
+def run_batch(tree: WaveletTree, batch: QueryBatch, workers: int = 1, *,
+              sort: bool = False) -> np.ndarray:
+    return BatchRunner(tree, batch.chunk_size, workers, sort=sort).run(batch)
 
 
 def access_batch(tree: WaveletTree, positions, workers: int = 1,
-                 chunk_size: int = DEFAULT_CHUNK_SIZE) -> np.ndarray:
+                 chunk_size: int = DEFAULT_CHUNK_SIZE, *, sort: bool = False) -> np.ndarray:
     """Batched access; original symbols in query order (batch.py:251-254)."""
-    return run_batch(tree, QueryBatch("access", positions, None, chunk_size), workers)
+    return run_batch(tree, QueryBatch("access", positions, None, chunk_size), workers, sort=sort)
 
 
 def rank_batch(tree: WaveletTree, symbols, positions, workers: int = 1,
-               chunk_size: int = DEFAULT_CHUNK_SIZE) -> np.ndarray:
+               chunk_size: int = DEFAULT_CHUNK_SIZE, *, sort: bool = False) -> np.ndarray:
     """Batched rank over (symbol, position) pairs (batch.py:257-260)."""
-    return run_batch(tree, QueryBatch("rank", positions, symbols, chunk_size), workers)
+    return run_batch(tree, QueryBatch("rank", positions, symbols, chunk_size), workers, sort=sort)
 
 
 def select_batch(tree: WaveletTree, symbols, ordinals, workers: int = 1,
-                 chunk_size: int = DEFAULT_CHUNK_SIZE) -> np.ndarray:
+                 chunk_size: int = DEFAULT_CHUNK_SIZE, *, sort: bool = False) -> np.ndarray:
     """Batched select over (symbol, ordinal) pairs (batch.py:263-266)."""
-    return run_batch(tree, QueryBatch("select", ordinals, symbols, chunk_size), workers)
+    return run_batch(tree, QueryBatch("select", ordinals, symbols, chunk_size), workers, sort=sort)

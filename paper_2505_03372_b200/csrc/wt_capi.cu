@@ -894,6 +894,13 @@ extern "C" int wt_tree_destroy(wt_tree* t) {
 // ---------------------------------------------------------------------------
 // queries
 // ---------------------------------------------------------------------------
+static u64 max_occ(const wt_tree* t) {
+  u64 mx = 1;
+  for (uint32_t i = 0; i < t->plan.sigma; ++i)
+    mx = std::max<u64>(mx, (u64)(t->plan.cum[i + 1] - t->plan.cum[i]));
+  return mx;
+}
+
 extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int64_t* args,
                              void* out, uint64_t m, uint64_t chunk, int flags, void* stream,
                              int64_t* bad_index, float* ms_out) {
@@ -918,8 +925,22 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
       CU(cudaEventCreate(&e1));
       CU(cudaEventRecord(e0, st));
     }
-    CU(launch_query(t->dev, kind, out_kind, validate, (const i64*)ids, (const i64*)args, out, m,
-                    t->rate_log, 0, t->bad, st));
+    if (flags & WT_F_SORT) {
+      Scratch S{{}, st};
+      QuerySortScratch Q{};
+      TRY(S.get(&Q.hist, 65536));
+      TRY(S.get(&Q.bucket_of, m));
+      TRY(S.get(&Q.ids_mapped, m));
+      TRY(S.get(&Q.sorted_ids, m));
+      TRY(S.get(&Q.sorted_args, m));
+      TRY(S.get(&Q.perm, m));
+      Q.max_occ = max_occ(t);
+      CU(launch_query_sorted(t->dev, kind, out_kind, validate, (const i64*)ids, (const i64*)args,
+                             out, m, t->rate_log, 0, t->bad, Q, st));
+    } else {
+      CU(launch_query(t->dev, kind, out_kind, validate, (const i64*)ids, (const i64*)args, out, m,
+                      t->rate_log, 0, t->bad, st));
+    }
     if (ms_out) CU(cudaEventRecord(e1, st));
     if (validate && bad_index)
       CU(cudaMemcpyAsync(bad_index, t->bad, 8, cudaMemcpyDeviceToHost, st));
@@ -938,7 +959,11 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
   // memory (the Python layer hands pinned result arrays for large batches).
   if (chunk == 0) chunk = 1ull << 22;
   if (chunk > m) chunk = m;
-  const size_t need = chunk * (16 + out_elem) + 64;
+  const bool sorted = (flags & WT_F_SORT) != 0;
+  // per slot: ids, args, out [+ sort scratch: buckets, bucket_of, mapped ids,
+  // sorted ids, sorted args, perm]
+  const size_t sort_bytes = sorted ? 65536 * 4 + chunk * (4 + 8 + 8 + 8 + 4) + 64 : 0;
+  const size_t need = chunk * (16 + out_elem) + 64 + sort_bytes;
   for (int i = 0; i < 3; ++i) {
     if (!t->qstream[i]) CU(cudaStreamCreateWithFlags(&t->qstream[i], cudaStreamNonBlocking));
     for (int j = 0; j < 2; ++j)
@@ -981,9 +1006,22 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sk, t->qev[0][s], 0);
     if (e == cudaSuccess && c >= 2) e = cudaStreamWaitEvent(sk, t->qev[2][s], 0);
     if (e == cudaSuccess && ms_out) e = cudaEventRecord(kt[2 * c], sk);
-    if (e == cudaSuccess)
+    if (e == cudaSuccess && !sorted) {
       e = launch_query(t->dev, kind, out_kind, validate, d_ids, d_args, d_out, cnt, t->rate_log, a,
                        t->bad, sk);
+    } else if (e == cudaSuccess) {
+      u8* sp = (u8*)(((uintptr_t)(d_out + chunk * out_elem) + 15) & ~(uintptr_t)15);
+      QuerySortScratch Q{};
+      Q.hist = (u32*)sp;
+      Q.ids_mapped = (i64*)(sp + 65536 * 4);
+      Q.sorted_ids = Q.ids_mapped + chunk;
+      Q.sorted_args = Q.sorted_ids + chunk;
+      Q.bucket_of = (u32*)(Q.sorted_args + chunk);
+      Q.perm = Q.bucket_of + chunk;
+      Q.max_occ = max_occ(t);
+      e = launch_query_sorted(t->dev, kind, out_kind, validate, d_ids, d_args, d_out, cnt,
+                              t->rate_log, a, t->bad, Q, sk);
+    }
     if (e == cudaSuccess && ms_out) e = cudaEventRecord(kt[2 * c + 1], sk);
     if (e == cudaSuccess) e = cudaEventRecord(t->qev[1][s], sk);
     // copy-out

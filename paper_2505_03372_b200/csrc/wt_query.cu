@@ -29,10 +29,12 @@ template <int kOut, bool kValidate>
 __global__ void __launch_bounds__(Q_NT) access_kernel(const __grid_constant__ TreeDev T,
                                                       const i64* __restrict__ pos,
                                                       void* __restrict__ out, u64 m, u64 base,
-                                                      u64* __restrict__ bad) {
-  const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
-  if (i >= m) return;
-  u64 p = (u64)pos[i];
+                                                      u64* __restrict__ bad,
+                                                      const u32* __restrict__ perm) {
+  const u64 q = (u64)blockIdx.x * Q_NT + threadIdx.x;
+  if (q >= m) return;
+  const u64 i = perm ? (u64)__ldg(perm + q) : q;  // result slot (sorted batches)
+  u64 p = (u64)pos[q];
   if (kValidate && p >= T.n) {  // negative positions wrap to huge values
     atomicMin(bad, base + i);
     return;
@@ -80,12 +82,14 @@ __global__ void __launch_bounds__(Q_NT) rank_kernel(const __grid_constant__ Tree
                                                     const i64* __restrict__ ids,
                                                     const i64* __restrict__ pos,
                                                     i64* __restrict__ out, u64 m, u64 base,
-                                                    u64* __restrict__ bad) {
-  const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
-  if (i >= m) return;
+                                                    u64* __restrict__ bad,
+                                                    const u32* __restrict__ perm) {
+  const u64 q = (u64)blockIdx.x * Q_NT + threadIdx.x;
+  if (q >= m) return;
+  const u64 i = perm ? (u64)__ldg(perm + q) : q;
   u32 c;
-  u64 p = (u64)pos[i];
-  if (!symbol_id<kValidate>(T, ids[i], c) || (kValidate && p > T.n)) {
+  u64 p = (u64)pos[q];
+  if (!symbol_id<kValidate>(T, ids[q], c) || (kValidate && p > T.n)) {
     atomicMin(bad, base + i);
     return;
   }
@@ -107,12 +111,14 @@ __global__ void __launch_bounds__(Q_NT) select_kernel(const __grid_constant__ Tr
                                                       const i64* __restrict__ ids,
                                                       const i64* __restrict__ ks,
                                                       i64* __restrict__ out, u64 m, int rate_log,
-                                                      u64 base, u64* __restrict__ bad) {
-  const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
-  if (i >= m) return;
+                                                      u64 base, u64* __restrict__ bad,
+                                                      const u32* __restrict__ perm) {
+  const u64 q = (u64)blockIdx.x * Q_NT + threadIdx.x;
+  if (q >= m) return;
+  const u64 i = perm ? (u64)__ldg(perm + q) : q;
   u32 c;
-  const i64 k = ks[i];
-  if (!symbol_id<kValidate>(T, ids[i], c) ||
+  const i64 k = ks[q];
+  if (!symbol_id<kValidate>(T, ids[q], c) ||
       (kValidate && (k < 1 || k > __ldg(T.cum + c + 1) - __ldg(T.cum + c)))) {
     atomicMin(bad, base + i);
     return;
@@ -134,38 +140,166 @@ __global__ void __launch_bounds__(Q_NT) select_kernel(const __grid_constant__ Tr
 
 template <bool V>
 static void launch_q(const TreeDev& T, int kind, int out_kind, const i64* ids, const i64* args,
-                     void* out, u64 m, int rate_log, u64 base, u64* bad, unsigned blocks,
-                     cudaStream_t st) {
+                     void* out, u64 m, int rate_log, u64 base, u64* bad, const u32* perm,
+                     unsigned blocks, cudaStream_t st) {
   switch (kind) {
     case 0:
       if (out_kind == 8)
-        access_kernel<8, V><<<blocks, Q_NT, 0, st>>>(T, args, out, m, base, bad);
+        access_kernel<8, V><<<blocks, Q_NT, 0, st>>>(T, args, out, m, base, bad, perm);
       else if (out_kind == 1)
-        access_kernel<1, V><<<blocks, Q_NT, 0, st>>>(T, args, out, m, base, bad);
+        access_kernel<1, V><<<blocks, Q_NT, 0, st>>>(T, args, out, m, base, bad, perm);
       else
-        access_kernel<2, V><<<blocks, Q_NT, 0, st>>>(T, args, out, m, base, bad);
+        access_kernel<2, V><<<blocks, Q_NT, 0, st>>>(T, args, out, m, base, bad, perm);
       break;
     case 1:
-      rank_kernel<V><<<blocks, Q_NT, 0, st>>>(T, ids, args, (i64*)out, m, base, bad);
+      rank_kernel<V><<<blocks, Q_NT, 0, st>>>(T, ids, args, (i64*)out, m, base, bad, perm);
       break;
     default:
-      select_kernel<V><<<blocks, Q_NT, 0, st>>>(T, ids, args, (i64*)out, m, rate_log, base, bad);
+      select_kernel<V><<<blocks, Q_NT, 0, st>>>(T, ids, args, (i64*)out, m, rate_log, base, bad, perm);
       break;
   }
 }
 
 cudaError_t launch_query(const TreeDev& T, int kind, int out_kind, bool validate, const i64* ids,
                          const i64* args, void* out, u64 m, int rate_log, u64 base, u64* bad,
-                         cudaStream_t st) {
+                         cudaStream_t st, const u32* perm) {
   if (m == 0) return cudaSuccess;
   if (kind < 0 || kind > 2) return cudaErrorInvalidValue;
   const u64 blocks = (m + Q_NT - 1) / Q_NT;
   if (blocks > 0x7fffffffull) return cudaErrorInvalidValue;
   if (validate)
-    launch_q<true>(T, kind, out_kind, ids, args, out, m, rate_log, base, bad, (unsigned)blocks, st);
+    launch_q<true>(T, kind, out_kind, ids, args, out, m, rate_log, base, bad, perm, (unsigned)blocks, st);
   else
-    launch_q<false>(T, kind, out_kind, ids, args, out, m, rate_log, base, bad, (unsigned)blocks, st);
+    launch_q<false>(T, kind, out_kind, ids, args, out, m, rate_log, base, bad, perm, (unsigned)blocks, st);
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// sort_queries_by_symbol on the device (batch.py:61-75):
+// a counting sort into at most 65,536 buckets -- (symbol id, coarse
+// position / ordinal) for rank / select, coarse position for access -- so
+// queries that walk the same nodes and nearby lines run side by side.
+// Results go back to query order through the permutation (the kernels'
+// `perm`).  Validation happens here, before anything runs (batch.py:112-148).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__ TreeDev T, int kind,
+                                                         const i64* __restrict__ ids,
+                                                         const i64* __restrict__ args, u64 m,
+                                                         bool validate, u32 bits_per_sym,
+                                                         u32 arg_shift, u32* __restrict__ bucket_of,
+                                                         i64* __restrict__ ids_out,
+                                                         u32* __restrict__ hist, u64 base,
+                                                         u64* __restrict__ bad) {
+  const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
+  if (i >= m) return;
+  const u64 a = (u64)args[i];
+  u32 bucket = 0;
+  bool ok = true;
+  if (kind == 0) {
+    ok = !validate || a < T.n;
+    bucket = ok ? (u32)(a >> arg_shift) : 0u;
+  } else {
+    u32 c = 0;
+    if (validate) {
+      const i64 raw = ids[i];
+      const int id = (raw < 0 || raw > 65535) ? -1 : __ldg(T.sym2id + raw);
+      ok = id >= 0;
+      c = ok ? (u32)id : 0u;
+    } else {
+      c = (u32)ids[i];
+    }
+    if (ok && validate) {
+      if (kind == 1) ok = a <= T.n;
+      else ok = a >= 1 && (i64)a <= __ldg(T.cum + c + 1) - __ldg(T.cum + c);
+    }
+    const u64 sub = kind == 1 ? a : a - 1;
+    bucket = ok ? (c << bits_per_sym) | (u32)(sub >> arg_shift) : 0u;
+    ids_out[i] = c;
+  }
+  if (!ok) atomicMin(bad, base + i);
+  bucket_of[i] = bucket;
+  atomicAdd(hist + bucket, 1u);
+}
+
+// one CTA: exclusive scan of the bucket counts in place
+__global__ void __launch_bounds__(1024) qsort_scan_kernel(u32* __restrict__ hist, u32 nb) {
+  __shared__ u32 wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 per = (nb + 1023) / 1024;
+  const u32 a = min(nb, tid * per), e = min(nb, a + per);
+  u32 sum = 0;
+  for (u32 i = a; i < e; ++i) sum += hist[i];
+  u32 inc = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    u32 v = wsum[lane];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v += y;
+    }
+    wsum[lane] = v;
+  }
+  __syncthreads();
+  u32 run = (warp ? wsum[warp - 1] : 0) + inc - sum;
+  for (u32 i = a; i < e; ++i) {
+    const u32 c = hist[i];
+    hist[i] = run;
+    run += c;
+  }
+}
+
+__global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restrict__ bucket_of,
+                                                             const i64* __restrict__ ids_in,
+                                                             const i64* __restrict__ args, u64 m,
+                                                             u32* __restrict__ cursor,
+                                                             i64* __restrict__ sids,
+                                                             i64* __restrict__ sargs,
+                                                             u32* __restrict__ perm) {
+  const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
+  if (i >= m) return;
+  const u32 slot = atomicAdd(cursor + bucket_of[i], 1u);
+  if (sids) sids[slot] = ids_in[i];
+  sargs[slot] = args[i];
+  perm[slot] = (u32)i;
+}
+
+cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool validate,
+                                const i64* ids, const i64* args, void* out, u64 m, int rate_log,
+                                u64 base, u64* bad, const QuerySortScratch& S, cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  if (m > 0xffffffffull) return cudaErrorInvalidValue;
+  const u64 blocks = (m + Q_NT - 1) / Q_NT;
+  // bucket layout: symbol bits + argument bits <= 16
+  u32 sym_bits = 0;
+  if (kind != 0)
+    while ((1u << sym_bits) < T.sigma) ++sym_bits;
+  const u32 bits_per_sym = 16 - sym_bits;
+  const u64 arg_span = kind == 2 ? S.max_occ : T.n + 1;  // args in [0, arg_span)
+  u32 arg_shift = 0;
+  while ((arg_span >> arg_shift) > (1ull << bits_per_sym)) ++arg_shift;
+  const u32 nb = 1u << 16;
+  cudaError_t e = cudaMemsetAsync(S.hist, 0, nb * 4, st);
+  if (e != cudaSuccess) return e;
+  qsort_key_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(T, kind, ids, args, m, validate, bits_per_sym,
+                                                      arg_shift, S.bucket_of, S.ids_mapped, S.hist,
+                                                      base, bad);
+  qsort_scan_kernel<<<1, 1024, 0, st>>>(S.hist, nb);
+  qsort_scatter_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(S.bucket_of, kind ? S.ids_mapped : nullptr,
+                                                          args, m, S.hist,
+                                                          kind ? S.sorted_ids : nullptr,
+                                                          S.sorted_args, S.perm);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // ids are mapped minimal ids now: run unvalidated (validation happened above)
+  return launch_query(T, kind, out_kind, false, S.sorted_ids, S.sorted_args, out, m, rate_log, base,
+                      bad, st, S.perm);
 }
 
 // ---------------------------------------------------------------------------

@@ -177,7 +177,7 @@ class WaveletTree:
                                lambda: bits.region_words(l), owner=handle)
 
     def query(self, kind: int, ids, args, *, symbols: bool = False, access_ids: bool = False,
-              chunk: int = 0):
+              chunk: int = 0, sort: bool = False):
         """Run one batch on the device; returns (out, first_bad_index)."""
         args = np.ascontiguousarray(np.asarray(args, np.int64).reshape(-1))
         m = len(args)
@@ -189,7 +189,8 @@ class WaveletTree:
             out = _lib.pinned_empty(m, np.int64)
         if m == 0:
             return out, -1
-        flags = (_lib.F_SYMBOLS if symbols else 0) | (_lib.F_ACCESS_IDS if access_ids else 0)
+        flags = ((_lib.F_SYMBOLS if symbols else 0) | (_lib.F_ACCESS_IDS if access_ids else 0)
+                 | (_lib.F_SORT if sort else 0))
         bad = C.c_int64(-1)
         check(lib.wt_tree_query(self._h.h, kind, ptr(ids_a), ptr(args), ptr(out), m, chunk,
                                 flags, None, C.byref(bad), None), "wt_tree_query")

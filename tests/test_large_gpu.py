@@ -87,3 +87,44 @@ def test_large_u8_text_u16_codes(W):
     o = O.build_with_alphabet(text, alpha)
     assert t.num_levels == 10
     assert_same_structure(t, o)
+
+
+@pytest.mark.parametrize("chunk", [1000, 1 << 16, 1 << 22])
+def test_device_query_sort_keeps_answers_and_errors(W, chunk):
+    """WT_F_SORT (device sort_queries_by_symbol): same answers in query order,
+    same first bad index, for every kind and chunking."""
+    text = np.random.default_rng(21).integers(0, 256, (1 << 20) + 17, dtype=np.uint8)
+    t = W.construct(text)
+    r = np.random.default_rng(22)
+    m = 50000
+    pos = r.integers(0, len(text), m)
+    syms = t.alphabet.sorted_symbols[r.integers(0, t.sigma, m)].astype(np.int64)
+    rpos = r.integers(0, len(text) + 1, m)
+    occ = np.diff(t.cum_hist)
+    ids = r.integers(0, t.sigma, m)
+    ks = 1 + (r.random(m) * occ[ids]).astype(np.int64)
+    ssym = t.alphabet.sorted_symbols[ids].astype(np.int64)
+    for f, args in ((W.access_batch, (pos,)), (W.rank_batch, (syms, rpos)),
+                    (W.select_batch, (ssym, ks))):
+        a = f(t, *args, chunk_size=chunk)
+        b = f(t, *args, chunk_size=chunk, sort=True)
+        assert np.array_equal(a, b)
+    bad = rpos.copy()
+    bad[[777, 31000]] = len(text) + 9
+    with pytest.raises(W.BatchError) as e1:
+        W.rank_batch(t, syms, bad, chunk_size=chunk, sort=True)
+    assert e1.value.index == 777
+    # device-resident path
+    import torch
+    from paper_2505_03372_b200 import _lib
+    import ctypes as C
+    d_ids = torch.from_numpy(ssym).cuda()
+    d_ks = torch.from_numpy(ks).cuda()
+    out = torch.empty(m, dtype=torch.int64, device="cuda")
+    badi = C.c_int64(-1)
+    _lib.check(_lib.lib.wt_tree_query(t.handle, _lib.Q_SELECT, C.c_void_p(d_ids.data_ptr()),
+                                      C.c_void_p(d_ks.data_ptr()), C.c_void_p(out.data_ptr()), m, 0,
+                                      _lib.F_DEVICE_PTRS | _lib.F_SYMBOLS | _lib.F_SORT, None,
+                                      C.byref(badi), None))
+    assert badi.value == -1
+    assert np.array_equal(out.cpu().numpy(), W.select_batch(t, ssym, ks))

@@ -32,7 +32,7 @@ class TextTree:
     def occurrences(self, c):
         return self.occ.get(int(c), 0)
 
-    def query(self, kind, ids, args, *, symbols=False, access_ids=False, chunk=0):
+    def query(self, kind, ids, args, *, symbols=False, access_ids=False, chunk=0, sort=False):
         args = np.asarray(args, np.int64)
         out = np.zeros(len(args), np.int64 if kind else self.text.dtype)
         for i, a in enumerate(args):

@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--sigma", type=int, default=256)
     ap.add_argument("--m", type=int, default=33_333_334)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--sort", action="store_true", help="WT_F_SORT: device sort by symbol")
     args = ap.parse_args()
     import torch
     import paper_2505_03372_b200 as W
@@ -42,7 +43,7 @@ def main():
     out_a = torch.empty(m, dtype=dt, device="cuda")
     out = torch.empty(m, dtype=torch.int64, device="cuda")
     st = torch.cuda.current_stream()
-    flags = _lib.F_DEVICE_PTRS | _lib.F_SYMBOLS
+    flags = _lib.F_DEVICE_PTRS | _lib.F_SYMBOLS | (_lib.F_SORT if args.sort else 0)
     bad = C.c_int64(-1)
     P = lambda t: C.c_void_p(t.data_ptr())
     for name, kind, ids, a, o in (("access", 0, None, pos, out_a), ("rank", 1, rsym, rpos, out),

@@ -667,6 +667,8 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
         CU(launch_wlevel(wp, in_bytes, P.code_bytes, l == 0 && dlut != nullptr, sm_count(device), st));
         ci ^= 1;
       }
+      // (the query-side layouts run after the last level: overlapping them
+      // with the next level's kernel on a side stream measured slower)
     } else {
     uint64_t max_tiles = 1;
     for (uint32_t l = 0; l < P.L; ++l)

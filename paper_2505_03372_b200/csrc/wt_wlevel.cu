@@ -41,6 +41,14 @@ constexpr int W_K = 4;         // 16-byte chunks per lane per tile
 #define WT_W_RING 2
 #endif
 constexpr int W_RING = WT_W_RING;  // input tiles in flight per warp
+#ifndef WT_W_NSTAGE
+#define WT_W_NSTAGE 1
+#endif
+constexpr int W_NSTAGE = WT_W_NSTAGE;  // staging buffers per warp (1 | 2)
+#ifndef WT_W_MINB
+#define WT_W_MINB 6
+#endif
+constexpr int W_MINB = WT_W_MINB;  // __launch_bounds__ min CTAs per SM
 constexpr unsigned FULLM = 0xffffffffu;
 
 template <typename TIn>
@@ -67,6 +75,9 @@ __device__ __forceinline__ void w_bulk_commit() {
 }
 __device__ __forceinline__ void w_bulk_wait_read1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void w_bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void w_bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -357,7 +368,7 @@ struct WF {
   static constexpr int ROWS = W_BYTES / 256;                 // 8
   static constexpr int WR = CR * (int)sizeof(TC) / 4;        // code words per lane-row
   static constexpr int STAGE = ((WS<TIn>::TILE * (int)sizeof(TC) + 64) + 127) & ~127;
-  static constexpr int WARP_SMEM = W_RING * W_BYTES + 2 * STAGE + 64;  // ring, stages, mbarriers
+  static constexpr int WARP_SMEM = W_RING * W_BYTES + W_NSTAGE * STAGE + 64;  // ring, stages, mbarriers
 };
 
 __device__ __forceinline__ void w_mbar_init(u64* bar) {
@@ -477,7 +488,7 @@ __device__ __forceinline__ void wcount_run3(const u8* stage, u32 soff, u32 cnt, 
 }
 
 template <typename TIn, typename TC, bool kLut>
-__global__ void __launch_bounds__(W_NT) wlevel_kernel(const __grid_constant__ WLevelParams P) {
+__global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_constant__ WLevelParams P) {
   using S = WS<TIn>;
   using F = WF<TIn, TC>;
   constexpr int TILE = S::TILE, TPL1 = S::TPL1;
@@ -490,7 +501,7 @@ __global__ void __launch_bounds__(W_NT) wlevel_kernel(const __grid_constant__ WL
   u8* wbase = smem_raw + 512 + warp * F::WARP_SMEM;
   u8* ring = wbase;
   u8* stage0 = wbase + W_RING * W_BYTES;
-  u64* mbar = reinterpret_cast<u64*>(wbase + W_RING * W_BYTES + 2 * F::STAGE);
+  u64* mbar = reinterpret_cast<u64*>(wbase + W_RING * W_BYTES + W_NSTAGE * F::STAGE);
 
   if (kLut && sizeof(TIn) == 1) {
     for (int i = tid; i < 256; i += W_NT) slut[i] = P.lut[i];
@@ -655,10 +666,12 @@ __global__ void __launch_bounds__(W_NT) wlevel_kernel(const __grid_constant__ WL
 
     if (scatter) {
       // ---- pass 2: stable partition into the staged zeros / ones runs ----------
-      u8* stage = stage0 + (it & 1) * F::STAGE;
+      u8* stage = stage0 + (W_NSTAGE == 2 ? (it & 1) : 0) * F::STAGE;
       const u32 sbase = smem_addr(stage);
-      if (it >= 2) {
-        if (lane == 0) w_bulk_wait_read1();  // the bulk store that last read this buffer
+      if (it >= (u32)W_NSTAGE) {
+        if (lane == 0) {  // the bulk store that last read this buffer
+          if (W_NSTAGE == 2) w_bulk_wait_read1(); else w_bulk_wait_read0();
+        }
         __syncwarp();
       }
       const u32 tile_zeros = TILE - tile_ones;

@@ -617,15 +617,15 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
         TRY(S.get(&tcnt[i], max_tiles + 64));
         TRY(S.get(&l1cnt[i], max_l1 + 4));
       }
+      // level-0 bit = top code bit = (symbol >= thr): codes are monotone in the symbol
+      uint32_t thr = 0x10000u;
+      for (uint32_t i = 0; i < P.sigma; ++i)
+        if ((P.values[i] >> (P.L - 1)) & 1u) {
+          thr = P.symbols[i];
+          break;
+        }
       if (P.L && P.sizes[0]) {
         CU(cudaMemsetAsync(l1cnt[0], 0, (t->lv[0].meta.n_l1 + 4) * 4, st));
-        // level-0 bit = top code bit = (symbol >= thr): codes are monotone in the symbol
-        uint32_t thr = 0x10000u;
-        for (uint32_t i = 0; i < P.sigma; ++i)
-          if ((P.values[i] >> (P.L - 1)) & 1u) {
-            thr = P.symbols[i];
-            break;
-          }
         CU(launch_wcount0(dtext, n, sym_bytes, thr, tcnt[0], l1cnt[0], sm_count(device), st));
       }
       int ci = 0;
@@ -659,6 +659,7 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
         wp.tile_counts = tcnt[ci];
         wp.next_tile_counts = tcnt[ci ^ 1];
         wp.next_l1_counts = l1cnt[ci ^ 1];
+        wp.thr = thr;
         wp.shift_bit = P.L - 1 - l;
         wp.shift_key = P.L - l;
         wp.l2_log = l2_log;

@@ -53,6 +53,7 @@ struct WLevelParams {
   const u32* tile_counts;  // ones per warp tile of this level
   u32* next_tile_counts;   // ones of level l+1 per warp tile of level l+1 (atomics)
   u32* next_l1_counts;     // ones of level l+1 per L1 block (atomics)
+  u32 thr;                 // level 0 with a LUT: smallest symbol whose code has the top bit
   u32 shift_bit;           // L-1-l
   u32 shift_key;           // L-l
   u32 l2_log;

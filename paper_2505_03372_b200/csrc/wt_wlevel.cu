@@ -574,9 +574,25 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
       const uint2 v = *reinterpret_cast<const uint2*>(tin + r * 256 + lane * 8);
-      u32 cw[WR];
-      wrow_codes<TIn, TC, kLut>(v, slut, P.lut, cw);
-      mrow[r] = wmask<TC, WR>(cw, P.shift_bit);
+      if (kLut) {
+        // level 0 through the LUT: the level bit is the TOP code bit, i.e.
+        // `symbol >= thr` (codes are monotone in symbols) -- a SIMD compare
+        // of the raw symbols, no table lookups in this pass
+        if (sizeof(TIn) == 1) {
+          const u32 t4 = P.thr * 0x01010101u;
+          const u32 y0 = __vcmpgeu4(v.x, t4) & 0x01010101u, y1 = __vcmpgeu4(v.y, t4) & 0x01010101u;
+          mrow[r] = P.thr > 0xffu ? 0u : ((y1 * 16u + y0) * 0x01020408u) >> 24;
+        } else {
+          const u32 t2 = P.thr * 0x00010001u;
+          const u32 y0 = __vcmpgeu2(v.x, t2) & 0x00010001u, y1 = __vcmpgeu2(v.y, t2) & 0x00010001u;
+          const u32 z = y1 * 4u + y0;  // bits 0, 16, 2, 18 -> elements 0, 1, 2, 3
+          mrow[r] = P.thr > 0xffffu ? 0u : (z | (z >> 15)) & 0xfu;
+        }
+      } else {
+        u32 cw[WR];
+        wrow_codes<TIn, TC, kLut>(v, slut, P.lut, cw);
+        mrow[r] = wmask<TC, WR>(cw, P.shift_bit);
+      }
     }
     u32 r1[ROWS], rtot[ROWS];
 #pragma unroll
@@ -686,14 +702,21 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
       for (int r = 0; r < ROWS; ++r) {
         const uint2 v = *reinterpret_cast<const uint2*>(tin + r * 256 + lane * 8);
         u32 cw[WR];
-        wrow_codes<TIn, TC, kLut>(v, slut, P.lut, cw);
+        if (!kLut) wrow_codes<TIn, TC, kLut>(v, slut, P.lut, cw);
         const u32 m = mrow[r];
         u32 oa = sbase + ooff + r1[r] * SZ;
         u32 za = sbase + zoff + ((u32)(r * RE + lane * CR) - r1[r]) * SZ;
 #pragma unroll
         for (int j = 0; j < CR; ++j) {
           // st.shared.u8/u16 keep the low bits: no masking of the element
-          const u32 val = sizeof(TC) == 1 ? cw[j >> 2] >> ((j & 3) * 8) : cw[j >> 1] >> ((j & 1) * 16);
+          u32 val;
+          if (kLut) {  // map each raw symbol as it is stored
+            const u32 raw = sizeof(TIn) == 1 ? ((j < 4 ? v.x : v.y) >> ((j & 3) * 8)) & 0xffu
+                                             : ((j < 2 ? v.x : v.y) >> ((j & 1) * 16)) & 0xffffu;
+            val = sizeof(TIn) == 1 ? (u32)slut[raw] : (u32)__ldg(P.lut + raw);
+          } else {
+            val = sizeof(TC) == 1 ? cw[j >> 2] >> ((j & 3) * 8) : cw[j >> 1] >> ((j & 1) * 16);
+          }
           if (m & (1u << j)) {
             st_shared<TC>(oa, val);
             oa += SZ;

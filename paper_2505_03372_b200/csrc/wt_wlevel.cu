@@ -105,10 +105,18 @@ __device__ __forceinline__ u32 wmask(const u32 (&cw)[WPC], u32 sh) {
       m |= ((y * 0x01020408u) >> 24) << (4 * (WPC - 1));
     }
   } else {
+    // two words (4 elements) per step: z = y0 + 4*y1 holds bits 0, 16, 2, 18
+    // for elements 0..3; (z | z >> 15) & 15 puts them in order
 #pragma unroll
-    for (int i = 0; i < WPC; ++i) {
-      const u32 y = (cw[i] >> sh) & 0x00010001u;
-      m |= ((y | (y >> 15)) & 3u) << (2 * i);
+    for (int i = 0; i + 1 < WPC; i += 2) {
+      const u32 y0 = (cw[i] >> sh) & 0x00010001u;
+      const u32 y1 = (cw[i + 1] >> sh) & 0x00010001u;
+      const u32 z = y1 * 4u + y0;
+      m |= ((z | (z >> 15)) & 15u) << (2 * i);
+    }
+    if (WPC & 1) {
+      const u32 y = (cw[WPC - 1] >> sh) & 0x00010001u;
+      m |= ((y | (y >> 15)) & 3u) << (2 * (WPC - 1));
     }
   }
   return m;

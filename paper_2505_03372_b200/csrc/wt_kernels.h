@@ -90,8 +90,8 @@ struct QuerySortScratch {
   u32* hist;        // 65536 bucket counts / cursors
   u32* bucket_of;   // m
   i64* ids_mapped;  // m (minimal ids)
-  i64* sorted_ids;  // m
-  i64* sorted_args; // m
+  i64* sorted_ids;  // unused (ids ride in sorted_args' top 16 bits)
+  i64* sorted_args; // m: argument | id << 48
   u32* perm;        // m
   u64 max_occ;      // largest symbol count (select ordinals are below it)
 };

@@ -17,6 +17,14 @@ namespace wt {
 
 constexpr int Q_NT = 256;
 
+// a sorted batch (WT_F_SORT) carries (argument | id << 48) per query
+// unpack the sorted batch (rank / select): id and argument
+__device__ __forceinline__ void qsort_unpack(i64 packed, u32& c, u64& a) {
+  c = (u32)((u64)packed >> 48);
+  a = (u64)packed & ((1ull << 48) - 1);
+}
+
+
 // Query batch contract (BatchRunner.run, batch.py:112-148 + :152-239):
 //   kValidate: `ids` holds ORIGINAL symbol values; each thread maps its symbol
 //   through sym2id and checks its argument range; an invalid query records
@@ -35,6 +43,7 @@ __global__ void __launch_bounds__(Q_NT) access_kernel(const __grid_constant__ Tr
   if (q >= m) return;
   const u64 i = perm ? (u64)__ldg(perm + q) : q;  // result slot (sorted batches)
   u64 p = (u64)pos[q];
+  if (perm) p = min(p & ((1ull << 48) - 1), T.n - 1);  // sorted batch: clamped in range
   if (kValidate && p >= T.n) {  // negative positions wrap to huge values
     atomicMin(bad, base + i);
     return;
@@ -88,10 +97,16 @@ __global__ void __launch_bounds__(Q_NT) rank_kernel(const __grid_constant__ Tree
   if (q >= m) return;
   const u64 i = perm ? (u64)__ldg(perm + q) : q;
   u32 c;
-  u64 p = (u64)pos[q];
-  if (!symbol_id<kValidate>(T, ids[q], c) || (kValidate && p > T.n)) {
-    atomicMin(bad, base + i);
-    return;
+  u64 p;
+  if (perm) {  // sorted batch: packed (position | id << 48), clamped in range
+    qsort_unpack(pos[q], c, p);
+    p = min(p, T.n);
+  } else {
+    p = (u64)pos[q];
+    if (!symbol_id<kValidate>(T, ids[q], c) || (kValidate && p > T.n)) {
+      atomicMin(bad, base + i);
+      return;
+    }
   }
   const u32 cd = __ldg(T.id_code + c);
   const u32 code = cd & 0xffffu, len = cd >> 16;
@@ -117,8 +132,13 @@ __global__ void __launch_bounds__(Q_NT) select_kernel(const __grid_constant__ Tr
   if (q >= m) return;
   const u64 i = perm ? (u64)__ldg(perm + q) : q;
   u32 c;
-  const i64 k = ks[q];
-  if (!symbol_id<kValidate>(T, ids[q], c) ||
+  i64 k;
+  if (perm) {  // sorted batch: packed (ordinal | id << 48), clamped in range
+    u64 a;
+    qsort_unpack(ks[q], c, a);
+    const i64 occ = __ldg(T.cum + c + 1) - __ldg(T.cum + c);
+    k = min(max((i64)a, (i64)1), max(occ, (i64)1));
+  } else if (k = ks[q], !symbol_id<kValidate>(T, ids[q], c) ||
       (kValidate && (k < 1 || k > __ldg(T.cum + c + 1) - __ldg(T.cum + c)))) {
     atomicMin(bad, base + i);
     return;
@@ -221,14 +241,21 @@ __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__
   atomicAdd(hist + bucket, 1u);
 }
 
-// one CTA: exclusive scan of the bucket counts in place
+// one CTA: exclusive scan of the 65536 bucket counts in place (64 per
+// thread, read as uint4 so the loads are independent)
 __global__ void __launch_bounds__(1024) qsort_scan_kernel(u32* __restrict__ hist, u32 nb) {
   __shared__ u32 wsum[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const u32 per = (nb + 1023) / 1024;
-  const u32 a = min(nb, tid * per), e = min(nb, a + per);
+  constexpr int PER = 64;  // nb == 65536
+  (void)nb;
+  uint4* h4 = reinterpret_cast<uint4*>(hist) + tid * (PER / 4);
+  uint4 v[PER / 4];
   u32 sum = 0;
-  for (u32 i = a; i < e; ++i) sum += hist[i];
+#pragma unroll
+  for (int k = 0; k < PER / 4; ++k) {
+    v[k] = h4[k];
+    sum += v[k].x + v[k].y + v[k].z + v[k].w;
+  }
   u32 inc = sum;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -238,35 +265,41 @@ __global__ void __launch_bounds__(1024) qsort_scan_kernel(u32* __restrict__ hist
   if (lane == 31) wsum[warp] = inc;
   __syncthreads();
   if (warp == 0) {
-    u32 v = wsum[lane];
+    u32 t = wsum[lane];
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const u32 y = __shfl_up_sync(0xffffffffu, v, d);
-      if (lane >= d) v += y;
+      const u32 y = __shfl_up_sync(0xffffffffu, t, d);
+      if (lane >= d) t += y;
     }
-    wsum[lane] = v;
+    wsum[lane] = t;
   }
   __syncthreads();
   u32 run = (warp ? wsum[warp - 1] : 0) + inc - sum;
-  for (u32 i = a; i < e; ++i) {
-    const u32 c = hist[i];
-    hist[i] = run;
-    run += c;
+#pragma unroll
+  for (int k = 0; k < PER / 4; ++k) {
+    uint4 o;
+    o.x = run; run += v[k].x;
+    o.y = run; run += v[k].y;
+    o.z = run; run += v[k].z;
+    o.w = run; run += v[k].w;
+    h4[k] = o;
   }
 }
 
+// the sorted batch: (argument | id << 48) and the query index -- 12 bytes
+// of scattered writes per query (ids ride in the argument's top bits:
+// positions / ordinals stay below 2^48)
 __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restrict__ bucket_of,
                                                              const i64* __restrict__ ids_in,
                                                              const i64* __restrict__ args, u64 m,
                                                              u32* __restrict__ cursor,
-                                                             i64* __restrict__ sids,
                                                              i64* __restrict__ sargs,
                                                              u32* __restrict__ perm) {
   const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
   if (i >= m) return;
   const u32 slot = atomicAdd(cursor + bucket_of[i], 1u);
-  if (sids) sids[slot] = ids_in[i];
-  sargs[slot] = args[i];
+  const u64 a = (u64)args[i] & ((1ull << 48) - 1);
+  sargs[slot] = (i64)(ids_in ? a | ((u64)ids_in[i] << 48) : a);
   perm[slot] = (u32)i;
 }
 
@@ -292,13 +325,13 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
                                                       base, bad);
   qsort_scan_kernel<<<1, 1024, 0, st>>>(S.hist, nb);
   qsort_scatter_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(S.bucket_of, kind ? S.ids_mapped : nullptr,
-                                                          args, m, S.hist,
-                                                          kind ? S.sorted_ids : nullptr,
-                                                          S.sorted_args, S.perm);
+                                                          args, m, S.hist, S.sorted_args, S.perm);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  // ids are mapped minimal ids now: run unvalidated (validation happened above)
-  return launch_query(T, kind, out_kind, false, S.sorted_ids, S.sorted_args, out, m, rate_log, base,
+  // ids are mapped minimal ids now (packed into the arguments): run
+  // unvalidated -- validation happened above; invalid queries are clamped
+  // into range by the walk and the batch raises anyway
+  return launch_query(T, kind, out_kind, false, nullptr, S.sorted_args, out, m, rate_log, base,
                       bad, st, S.perm);
 }
 

@@ -620,8 +620,10 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
       rtot[r + 1] = tot >> 16;
     }
     u32 tile_ones = 0;
+    u32 rstart[ROWS];  // ones of the tile before row r (warp-uniform)
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
+      rstart[r] = tile_ones;
       r1[r] += tile_ones;
       tile_ones += rtot[r];
     }
@@ -641,12 +643,9 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
 
     // ---- L2 entries: blocks start at lane-row boundaries (l2_bits >= 64) ------
     if ((1u << P.l2_log) >= (u32)RE) {  // at most one per row: lane r handles row r
-      u32 rs = 0;  // ones before row `lane` (= r1 of lane 0 in that row)
+      u32 rs = 0;  // ones before row `lane`
 #pragma unroll
-      for (int r = 0; r < ROWS; ++r) {
-        const u32 v = __shfl_sync(FULLM, r1[r], 0);
-        rs = lane == r ? v : rs;
-      }
+      for (int r = 0; r < ROWS; ++r) rs = lane == r ? rstart[r] : rs;
       const u64 g = t0 + (u64)lane * RE;
       if (lane < ROWS && (((u32)g) & ((1u << P.l2_log) - 1)) == 0)
         P.l2[g >> P.l2_log] = (u16)(P1 + rs - l1v);
@@ -668,19 +667,22 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
       if (q0 > base + cnt) continue;
       for (u64 qo = q0; qo <= base + cnt; qo += P.rate) {
         const u32 tt = (u32)(qo - base);  // 1-based ordinal inside the tile
-        u32 pre_l = 0, mk = 0, rr = 0;
-        bool own = false;
+        // the row holding ordinal tt (warp-uniform), then its lane (ballot)
+        u32 rr = 0;
 #pragma unroll
-        for (int r = 0; r < ROWS; ++r) {
-          const u32 pl = ones ? r1[r] : (u32)(r * RE + lane * CR) - r1[r];
-          const u32 mr = ones ? mrow[r] : (~mrow[r] & ((1u << CR) - 1u));
-          if (!own && pl < tt && tt <= pl + __popc(mr)) {
-            own = true;
-            pre_l = pl;
-            mk = mr;
-            rr = r;
-          }
+        for (int r = 1; r < ROWS; ++r) {
+          const u32 before = ones ? rstart[r] : (u32)(r * RE) - rstart[r];
+          rr = before < tt ? (u32)r : rr;
         }
+        u32 r1s = r1[0], ms = mrow[0];
+#pragma unroll
+        for (int r = 1; r < ROWS; ++r) {
+          r1s = rr == (u32)r ? r1[r] : r1s;
+          ms = rr == (u32)r ? mrow[r] : ms;
+        }
+        const u32 pre_l = ones ? r1s : rr * RE + lane * CR - r1s;
+        const u32 mk = ones ? ms : (~ms & ((1u << CR) - 1u));
+        const bool own = pre_l < tt && tt <= pre_l + __popc(mk);
         if (own) {
           const u64 sidx = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
           if (sidx < cap) out[sidx] = t0 + rr * RE + lane * CR + select_in_word32(mk, tt - pre_l);

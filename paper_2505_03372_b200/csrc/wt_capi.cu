@@ -929,17 +929,22 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
       CU(cudaEventRecord(e0, st));
     }
     if (flags & WT_F_SORT) {
+      // sorted in slices of at most 2^31 queries (u32 permutation indices)
+      const uint64_t slice = std::min<uint64_t>(m, 1ull << 31);
       Scratch S{{}, st};
       QuerySortScratch Q{};
       TRY(S.get(&Q.hist, 65536));
-      TRY(S.get(&Q.bucket_of, m));
-      TRY(S.get(&Q.ids_mapped, m));
-      TRY(S.get(&Q.sorted_ids, m));
-      TRY(S.get(&Q.sorted_args, m));
-      TRY(S.get(&Q.perm, m));
+      TRY(S.get(&Q.bucket_of, slice));
+      TRY(S.get(&Q.ids_mapped, slice));
+      TRY(S.get(&Q.sorted_args, slice));
+      TRY(S.get(&Q.perm, slice));
       Q.max_occ = max_occ(t);
-      CU(launch_query_sorted(t->dev, kind, out_kind, validate, (const i64*)ids, (const i64*)args,
-                             out, m, t->rate_log, 0, t->bad, Q, st));
+      for (uint64_t a = 0; a < m; a += slice) {
+        const uint64_t cnt = std::min(slice, m - a);
+        CU(launch_query_sorted(t->dev, kind, out_kind, validate,
+                               ids ? (const i64*)ids + a : nullptr, (const i64*)args + a,
+                               (u8*)out + a * out_elem, cnt, t->rate_log, a, t->bad, Q, st));
+      }
     } else {
       CU(launch_query(t->dev, kind, out_kind, validate, (const i64*)ids, (const i64*)args, out, m,
                       t->rate_log, 0, t->bad, st));

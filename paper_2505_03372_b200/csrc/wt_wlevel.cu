@@ -448,50 +448,100 @@ __device__ __forceinline__ u32 wswar16(uint4 v, u32 sh) {
   return (y * 0x00010001u) >> 16;
 }
 
-// next-level ones of one staged run (elements [0, cnt) at stage byte soff),
-// per next-level tile (a run spans at most 3) and L1 block.  Returns the
-// three counts (lanes hold the sums): prefix counts up to the tile boundaries
-// b1, b2 give the split.  16-byte aligned chunks fully inside the run are
-// counted with SWAR; the few elements outside them (run head / tail) and the
-// parts of the chunks holding b1 / b2 are counted one element per lane.
+// one element of a staged run, next-level bit
 template <typename TC>
-__device__ __forceinline__ void wcount_run3(const u8* stage, u32 soff, u32 cnt, u32 b1, u32 b2,
-                                            u32 sh1, int lane, u32& ca, u32& cp1, u32& cp2) {
+__device__ __forceinline__ u32 wbit_at(const u8* stage, u32 byte, u32 sh) {
+  const u32 v = sizeof(TC) == 1 ? (u32)stage[byte] : (u32)*reinterpret_cast<const u16*>(stage + byte);
+  return (v >> sh) & 1u;
+}
+
+// next-level ones of the zeros run (Z elements at stage byte zoff, global
+// destination zdst) and of the ones run (O at ooff, odst), per next-level tile
+// (a run spans <= 3) and L1 block.  One pass over the aligned 16-byte chunks
+// of both runs (SWAR), element-wise passes for the run heads / tails and for
+// the parts of the chunks holding a tile boundary; prefix counts up to the
+// boundaries give the split.  Lanes 0..5 add the six counts.
+template <typename TC>
+__device__ __forceinline__ void wcount_tile(const u8* stage, u32 Z, u32 zoff, u64 zdst, u32 O,
+                                            u32 ooff, u64 odst, u32 sh, int tile_log,
+                                            u32* tcounts, u32* l1counts, int lane) {
   constexpr u32 SZ = sizeof(TC);
   constexpr u32 EPC = 16 / SZ;
-  const u32 h = min(cnt, ((16u - (soff & 15u)) & 15u) / SZ);  // head elements
-  const u32 nfull = (cnt - h) / EPC;
-  const u32 ts = h + nfull * EPC;                               // tail start
-  const u8* base = stage + soff;
-  for (u32 c = lane; c < nfull; c += 32) {
-    const u32 i0 = h + c * EPC;
-    const u32 x = wswar16<TC>(*reinterpret_cast<const uint4*>(base + i0 * SZ), sh1);
-    ca += x;
-    cp1 += i0 + EPC <= b1 ? x : 0u;
-    cp2 += i0 + EPC <= b2 ? x : 0u;
+  const u64 nt = 1ull << tile_log;
+  // per run: head elements h, full chunks nf, tail start ts, boundaries b1 <= b2
+  const u32 hz = min(Z, ((16u - (zoff & 15u)) & 15u) / SZ), nfz = (Z - hz) / EPC, tsz = hz + nfz * EPC;
+  const u32 ho = min(O, ((16u - (ooff & 15u)) & 15u) / SZ), nfo = (O - ho) / EPC, tso = ho + nfo * EPC;
+  const u32 b1z = min(Z, (u32)((((zdst >> tile_log) + 1) << tile_log) - zdst)), b2z = min(Z, b1z + (u32)nt);
+  const u32 b1o = min(O, (u32)((((odst >> tile_log) + 1) << tile_log) - odst)), b2o = min(O, b1o + (u32)nt);
+  u32 az = 0, p1z = 0, p2z = 0, ao = 0, p1o = 0, p2o = 0;
+  for (u32 c = lane; c < nfz + nfo; c += 32) {
+    const bool one = c >= nfz;
+    const u32 i0 = one ? ho + (c - nfz) * EPC : hz + c * EPC;
+    const u32 x = wswar16<TC>(*reinterpret_cast<const uint4*>(stage + (one ? ooff : zoff) + i0 * SZ), sh);
+    const u32 e = i0 + EPC;
+    if (one) {
+      ao += x;
+      p1o += e <= b1o ? x : 0u;
+      p2o += e <= b2o ? x : 0u;
+    } else {
+      az += x;
+      p1z += e <= b1z ? x : 0u;
+      p2z += e <= b2z ? x : 0u;
+    }
   }
-  // element-wise: lanes 0..15 head, 16..31 tail (count toward ca, cp1, cp2)
-  {
-    const u32 k = lane & 15;
-    const u32 i = lane < 16 ? k : ts + k;
-    const bool in = lane < 16 ? k < h : i < cnt;
-    const u32 v = in ? (SZ == 1 ? (u32)base[i] : (u32)reinterpret_cast<const u16*>(base)[i]) : 0u;
-    const u32 bt = in ? (v >> sh1) & 1u : 0u;
-    ca += bt;
-    cp1 += i < b1 ? bt : 0u;
-    cp2 += i < b2 ? bt : 0u;
+  // element-wise 1: heads and tails (lanes 0-7 z head, 8-15 z tail, 16-23 o head, 24-31 o tail;
+  // EPC <= 16 so each is < 16 elements: two rounds)
+#pragma unroll
+  for (int rnd = 0; rnd < 2; ++rnd) {
+    const u32 k = (lane & 7) + 8 * rnd;
+    const bool one = lane >= 16, tail = (lane & 8) != 0;
+    const u32 cnt = one ? O : Z, h = one ? ho : hz, ts = one ? tso : tsz;
+    const u32 i = tail ? ts + k : k;
+    const bool in = tail ? i < cnt : k < h;
+    const u32 bt = in ? wbit_at<TC>(stage, (one ? ooff : zoff) + i * SZ, sh) : 0u;
+    const u32 b1 = one ? b1o : b1z, b2 = one ? b2o : b2z;
+    if (one) {
+      ao += bt; p1o += i < b1 ? bt : 0u; p2o += i < b2 ? bt : 0u;
+    } else {
+      az += bt; p1z += i < b1 ? bt : 0u; p2z += i < b2 ? bt : 0u;
+    }
   }
-  // element-wise: the part before b1 (lanes 0..15) / b2 (lanes 16..31) of
-  // the full chunk holding that boundary (those chunks were not added)
-  {
-    const u32 bb = lane < 16 ? b1 : b2;
+  // element-wise 2: the part before each boundary of the full chunk holding it
+  // (lanes 0-7 b1z, 8-15 b2z, 16-23 b1o, 24-31 b2o; two rounds)
+#pragma unroll
+  for (int rnd = 0; rnd < 2; ++rnd) {
+    const u32 k = (lane & 7) + 8 * rnd;
+    const bool one = lane >= 16, second = (lane & 8) != 0;
+    const u32 h = one ? ho : hz, ts = one ? tso : tsz;
+    const u32 bb = one ? (second ? b2o : b1o) : (second ? b2z : b1z);
     const bool strad = bb > h && bb < ts && ((bb - h) % EPC) != 0;
-    const u32 cs = strad ? h + ((bb - h) / EPC) * EPC : 0u;
-    const u32 i = cs + (lane & 15);
+    const u32 i = (strad ? h + ((bb - h) / EPC) * EPC : 0u) + k;
     const bool in = strad && i < bb;
-    const u32 v = in ? (SZ == 1 ? (u32)base[i] : (u32)reinterpret_cast<const u16*>(base)[i]) : 0u;
-    const u32 bt = in ? (v >> sh1) & 1u : 0u;
-    if (lane < 16) cp1 += bt; else cp2 += bt;
+    const u32 bt = in ? wbit_at<TC>(stage, (one ? ooff : zoff) + i * SZ, sh) : 0u;
+    if (one) {
+      if (second) p2o += bt; else p1o += bt;
+    } else {
+      if (second) p2z += bt; else p1z += bt;
+    }
+  }
+  u32 q0 = az | (ao << 16), q1 = p1z | (p1o << 16), q2 = p2z | (p2o << 16);  // counts <= 4096
+#pragma unroll
+  for (int d = 16; d; d >>= 1) {
+    q0 += __shfl_xor_sync(FULLM, q0, d);
+    q1 += __shfl_xor_sync(FULLM, q1, d);
+    q2 += __shfl_xor_sync(FULLM, q2, d);
+  }
+  if (lane < 6) {
+    const bool one = lane >= 3;
+    const int seg = lane - (one ? 3 : 0);
+    const u32 sft = one ? 16 : 0;
+    const u32 a = (q0 >> sft) & 0xffffu, c1 = (q1 >> sft) & 0xffffu, c2 = (q2 >> sft) & 0xffffu;
+    const u32 cc = seg == 0 ? c1 : seg == 1 ? c2 - c1 : a - c2;
+    if (cc) {
+      const u64 tf = ((one ? odst : zdst) >> tile_log) + seg;
+      atomicAdd(tcounts + tf, cc);
+      atomicAdd(l1counts + ((tf << tile_log) >> 16), cc);
+    }
   }
 }
 
@@ -761,28 +811,11 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
           gout[db + o2] = stage[soff + o2];
         }
         if (lane == 0 && body) w_bulk_s2g(gout + db + head, stage + soff + head, body);
-        // next level's ones of this run per next-level tile (<= 3) and L1 block
-        const u64 t_first = dst >> NTILE_LOG;
-        const u32 b1 = min(cnt, (u32)(((t_first + 1) << NTILE_LOG) - dst));
-        const u32 b2 = min(cnt, b1 + (1u << NTILE_LOG));
-        u32 ca = 0, cp1 = 0, cp2 = 0;
-        wcount_run3<TC>(stage, soff, cnt, b1, b2, P.shift_bit - 1, lane, ca, cp1, cp2);
-        u32 pk = cp1 | (cp2 << 16);  // counts <= 4096 fit in 16 bits
-#pragma unroll
-        for (int d = 16; d; d >>= 1) {
-          ca += __shfl_xor_sync(FULLM, ca, d);
-          pk += __shfl_xor_sync(FULLM, pk, d);
-        }
-        if (lane < 3) {
-          const u32 p1 = pk & 0xffffu, p2 = pk >> 16;
-          const u32 cc = lane == 0 ? p1 : lane == 1 ? p2 - p1 : ca - p2;
-          if (cc) {
-            const u64 tf = t_first + lane;
-            atomicAdd(P.next_tile_counts + tf, cc);
-            atomicAdd(P.next_l1_counts + ((tf << NTILE_LOG) >> 16), cc);
-          }
-        }
       }
+      // next level's ones of both runs per next-level tile (<= 3 per run) and
+      // L1 block, in one pass over the staged tile
+      wcount_tile<TC>(stage, zlive ? tile_zeros : 0u, zoff, zdst, olive ? tile_ones : 0u, ooff, odst,
+                      P.shift_bit - 1, NTILE_LOG, P.next_tile_counts, P.next_l1_counts, lane);
       if (lane == 0) w_bulk_commit();  // one bulk group per scattering fast tile
     } else {
       __syncwarp();

@@ -979,16 +979,23 @@ __global__ void __launch_bounds__(256) wcount0_kernel(const TIn* __restrict__ te
 }
 
 // one CTA: exclusive scan of per-L1-block counts -> the level's L1 directory
-// (ones before each 65536-bit block) and its total
+// (ones before each 65536-bit block) and its total.  Each thread owns a
+// contiguous run of blocks read as uint4 (counts are padded to a multiple of
+// 4 with zeros by the caller's memset).
 __global__ void __launch_bounds__(1024) l1_scan_kernel(const u32* __restrict__ counts, u64 n_l1,
                                                        u64* __restrict__ l1, u64* __restrict__ total) {
   __shared__ u64 wsum[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const u64 per = (n_l1 + 1023) / 1024;
-  const u64 a = min(n_l1, (u64)tid * per), e = min(n_l1, a + per);
+  const u64 quads = (n_l1 + 3) / 4;
+  const u64 per = (quads + 1023) / 1024;  // quads per thread
+  const u64 a = min(quads, (u64)tid * per), e = min(quads, a + per);
+  const uint4* c4 = reinterpret_cast<const uint4*>(counts);
   u64 s = 0;
-#pragma unroll 8
-  for (u64 i = a; i < e; ++i) s += __ldg(counts + i);
+#pragma unroll 4
+  for (u64 q = a; q < e; ++q) {
+    const uint4 v = __ldg(c4 + q);
+    s += (u64)v.x + v.y + v.z + v.w;
+  }
   u64 inc = s;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -1008,10 +1015,15 @@ __global__ void __launch_bounds__(1024) l1_scan_kernel(const u32* __restrict__ c
   }
   __syncthreads();
   u64 run = (warp ? wsum[warp - 1] : 0) + inc - s;
-#pragma unroll 8
-  for (u64 i = a; i < e; ++i) {
-    l1[i] = run;
-    run += __ldg(counts + i);
+#pragma unroll 4
+  for (u64 q = a; q < e; ++q) {
+    const uint4 v = __ldg(c4 + q);
+    const u32 cv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (q * 4 + j < n_l1) l1[q * 4 + j] = run;
+      run += cv[j];
+    }
   }
   if (tid == 1023) *total = wsum[31];
 }

@@ -35,8 +35,6 @@ namespace {
 
 constexpr int W_NT = 128;
 constexpr int W_WARPS = W_NT / 32;
-constexpr int W_BYTES = 2048;  // input bytes per warp tile
-constexpr int W_K = 4;         // 16-byte chunks per lane per tile
 #ifndef WT_W_RING
 #define WT_W_RING 2
 #endif
@@ -51,15 +49,16 @@ constexpr int W_NSTAGE = WT_W_NSTAGE;  // staging buffers per warp (1 | 2)
 constexpr int W_MINB = WT_W_MINB;  // __launch_bounds__ min CTAs per SM
 constexpr unsigned FULLM = 0xffffffffu;
 
+// a warp tile is 2048 elements for both input widths (2 KiB of u8 / 4 KiB
+// of u16), so per-tile costs are amortized alike and every level's tile
+// counts have the same granularity
 template <typename TIn>
 struct WS {
-  static constexpr int CH = 16 / (int)sizeof(TIn);         // elements per chunk
-  static constexpr int TILE = W_BYTES / (int)sizeof(TIn);  // 2048 | 1024
-  static constexpr int TPL1 = kL1Bits / TILE;              // 32 | 64 tiles per L1 block
-};
-template <typename TIn, typename TC>
-struct WStage {
-  static constexpr int BYTES = WS<TIn>::TILE * (int)sizeof(TC) + 64;
+  static constexpr int CH = 16 / (int)sizeof(TIn);          // elements per 16-byte chunk
+  static constexpr int TILE = 2048;                         // elements per warp tile
+  static constexpr int BYTES = TILE * (int)sizeof(TIn);     // 2048 | 4096
+  static constexpr int K = BYTES / 512;                     // 16-byte chunks per lane (4 | 8)
+  static constexpr int TPL1 = kL1Bits / TILE;               // 32 tiles per L1 block
 };
 
 __device__ __forceinline__ u32 smem_addr(const void* p) {
@@ -163,17 +162,18 @@ __device__ __forceinline__ uint4 w_load16(const void* p) {
 
 // load one tile's 4 chunks per lane; bytes beyond the level are zero
 template <typename TIn>
-__device__ __forceinline__ void wload(const u8* in, u64 m, u32 t, int lane, uint4 (&q)[W_K]) {
+__device__ __forceinline__ void wload(const u8* in, u64 m, u32 t, int lane,
+                                      uint4 (&q)[WS<TIn>::K]) {
   using S = WS<TIn>;
   const u64 t0 = (u64)t * S::TILE;
   const u8* base = in + t0 * sizeof(TIn);
   if (t0 + S::TILE <= m) {
 #pragma unroll
-    for (int k = 0; k < W_K; ++k) q[k] = w_load16(base + (k * 32 + lane) * 16);
+    for (int k = 0; k < S::K; ++k) q[k] = w_load16(base + (k * 32 + lane) * 16);
   } else {
     const u64 bytes = (m - t0) * sizeof(TIn);
 #pragma unroll
-    for (int k = 0; k < W_K; ++k) {
+    for (int k = 0; k < S::K; ++k) {
       const u32 o = (u32)(k * 32 + lane) * 16;
       if (o + 16 <= bytes) {
         q[k] = w_load16(base + o);
@@ -201,16 +201,16 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
   using S = WS<TIn>;
   constexpr int CH = S::CH, TILE = S::TILE, TPL1 = S::TPL1;
   constexpr int WPC = CH * (int)sizeof(TC) / 4;
-  constexpr int NTILE_LOG = sizeof(TC) == 1 ? 11 : 10;
+  constexpr int NTILE_LOG = 11;  // next level's tile: 2048 elements
   const int lane = threadIdx.x & 31;
   const bool scatter = P.out != nullptr;
   const u8* in = reinterpret_cast<const u8*>(P.in);
   const u32 l2_chunks = (1u << P.l2_log) / CH;
-  uint4 q[W_K];
+  uint4 q[S::K];
   wload<TIn>(in, P.m, t, lane, q);
-  u32 cw[W_K][WPC];
+  u32 cw[S::K][WPC];
 #pragma unroll
-  for (int k = 0; k < W_K; ++k) wcodes<TIn, TC, kLut, WPC>(q[k], slut, P.lut, cw[k]);
+  for (int k = 0; k < S::K; ++k) wcodes<TIn, TC, kLut, WPC>(q[k], slut, P.lut, cw[k]);
     const u64 t0 = (u64)t * TILE;
     const u32 valid = (u32)min((u64)TILE, P.m - t0);
     // ---- P1: ones before the tile ------------------------------------------
@@ -228,17 +228,17 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
     const u64 P1 = l1v + pre;
 
     // ---- 1. codes, masks, in-tile scan ---------------------------------------
-    u32 msk[W_K];
+    u32 msk[S::K];
 #pragma unroll
-    for (int k = 0; k < W_K; ++k) {
+    for (int k = 0; k < S::K; ++k) {
       u32 mk = wmask<TC, WPC>(cw[k], P.shift_bit);
       const u32 e = (u32)(k * 32 + lane) * CH;
       if (e + CH > valid) mk &= e >= valid ? 0u : (1u << (valid - e)) - 1u;
       msk[k] = mk;
     }
-    u32 r1c[W_K], ktot[W_K];
+    u32 r1c[S::K], ktot[S::K];
 #pragma unroll
-    for (int k = 0; k < W_K; k += 2) {
+    for (int k = 0; k < S::K; k += 2) {
       const u32 x = (u32)__popc(msk[k]) | ((u32)__popc(msk[k + 1]) << 16);
       u32 inc = x;
 #pragma unroll
@@ -255,14 +255,14 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
     }
     u32 tile_ones = 0;
 #pragma unroll
-    for (int k = 0; k < W_K; ++k) {
+    for (int k = 0; k < S::K; ++k) {
       r1c[k] += tile_ones;
       tile_ones += ktot[k];
     }
 
     // ---- bit-vector words -----------------------------------------------------
 #pragma unroll
-    for (int k = 0; k < W_K; ++k) {
+    for (int k = 0; k < S::K; ++k) {
       const u32 e = (u32)(k * 32 + lane) * CH;
       if (e < ((valid + 63u) & ~63u)) {  // through the level's last word: padding stays zero
         const u64 bit = t0 + e;
@@ -277,7 +277,7 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
     if (l2_chunks <= 32) {
       if ((lane & (l2_chunks - 1)) == 0) {
 #pragma unroll
-        for (int k = 0; k < W_K; ++k) {
+        for (int k = 0; k < S::K; ++k) {
           const u32 e = (u32)(k * 32 + lane) * CH;
           if (e < valid) P.l2[(t0 + e) >> P.l2_log] = (u16)(P1 + r1c[k] - l1v);
         }
@@ -285,7 +285,7 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
     } else if (lane == 0) {
       const u64 l2m = (1ull << P.l2_log) - 1;
 #pragma unroll
-      for (int k = 0; k < W_K; ++k) {
+      for (int k = 0; k < S::K; ++k) {
         const u64 g = t0 + (u64)k * 32 * CH;
         if (g < P.m && (g & l2m) == 0) P.l2[g >> P.l2_log] = (u16)(P1 + r1c[k] - l1v);
       }
@@ -301,9 +301,9 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
       const u64 cap = ones ? P.ones_cap : P.zeros_cap;
       for (u64 qo = wnext_multiple(base, P.rate, P.rate_log); qo <= base + cnt; qo += P.rate) {
         const u32 tt = (u32)(qo - base);  // 1-based ordinal inside the tile
-        u32 kk = W_K - 1, acc = 0;  // k-row holding ordinal tt
+        u32 kk = S::K - 1, acc = 0;  // k-row holding ordinal tt
 #pragma unroll
-        for (int k = 0; k < W_K; ++k) {
+        for (int k = 0; k < S::K; ++k) {
           const int rv = (int)valid - k * 32 * CH;
           const u32 row_valid = rv <= 0 ? 0u : (rv >= 32 * CH ? 32u * CH : (u32)rv);
           const u32 kc = ones ? ktot[k] : row_valid - ktot[k];
@@ -313,7 +313,7 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
         // lane owning ordinal tt within k-row kk
         u32 pre_l = 0, cnt_l = 0, mk = 0;
 #pragma unroll
-        for (int k = 0; k < W_K; ++k) {
+        for (int k = 0; k < S::K; ++k) {
           if ((u32)k == kk) {
             const u32 e = (u32)(k * 32 + lane) * CH;
             const u32 vm = e >= valid ? 0u : (e + CH <= valid ? (CH == 16 ? 0xffffu : 0xffu)
@@ -337,11 +337,14 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
       TC* gout = reinterpret_cast<TC*>(P.out);
       const u32 sh1 = P.shift_bit - 1;
 #pragma unroll
-      for (int k = 0; k < W_K; ++k) {
+      for (int k = 0; k < S::K; ++k) {
         const u32 e = (u32)(k * 32 + lane) * CH;
         u32 r1 = r1c[k];
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
+          // next-level ones, warp-aggregated per destination tile: lanes
+          // whose element lands in the same next-level tile add together
+          u32 tf = 0xffffffffu;
           if (e + j < valid) {
             const u32 v = welem<TC, WPC>(cw[k], j);
             const NodeEnt* ne = P.nodes + (v >> P.shift_key);
@@ -350,12 +353,15 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
                                : (u64)__ldg(&ne->zero_base) + (t0 + e + j - P1 - r1);
             if (dst < P.m_next) {
               gout[dst] = (TC)v;
-              if ((v >> sh1) & 1u) {
-                atomicAdd(P.next_tile_counts + (dst >> NTILE_LOG), 1u);
-                atomicAdd(P.next_l1_counts + (dst >> 16), 1u);
-              }
+              if ((v >> sh1) & 1u) tf = (u32)(dst >> NTILE_LOG);
             }
             r1 += bt;
+          }
+          const u32 key = tf != 0xffffffffu ? tf : 0x80000000u | (u32)lane;  // unique if none
+          const unsigned peers = __match_any_sync(FULLM, key);
+          if (tf != 0xffffffffu && lane == __ffs(peers) - 1) {
+            atomicAdd(P.next_tile_counts + tf, (u32)__popc(peers));
+            atomicAdd(P.next_l1_counts + (((u64)tf << NTILE_LOG) >> 16), (u32)__popc(peers));
           }
         }
       }
@@ -371,25 +377,28 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
 // step fall in distinct banks.
 template <typename TIn, typename TC>
 struct WF {
-  static constexpr int CR = 8 / (int)sizeof(TIn);            // elements per lane per row
-  static constexpr int RE = 256 / (int)sizeof(TIn);          // elements per row
-  static constexpr int ROWS = W_BYTES / 256;                 // 8
+  static constexpr int CR = 8;                               // elements per lane per row
+  static constexpr int RE = 256;                             // elements per row
+  static constexpr int ROWS = WS<TIn>::TILE / RE;            // 8
+  static constexpr int LB = CR * (int)sizeof(TIn);           // input bytes per lane-row (8 | 16)
+  static constexpr int LW = LB / 4;                          // input words per lane-row
+  static constexpr int RB = 32 * LB;                         // input bytes per row
   static constexpr int WR = CR * (int)sizeof(TC) / 4;        // code words per lane-row
-  static constexpr int STAGE = ((WS<TIn>::TILE * (int)sizeof(TC) + 64) + 127) & ~127;
-  static constexpr int WARP_SMEM = W_RING * W_BYTES + W_NSTAGE * STAGE + 64;  // ring, stages, mbarriers
+  static constexpr int STAGE = ((WS<TIn>::TILE * (int)sizeof(TC) + 128) + 127) & ~127;  // 4 runs
+  static constexpr int WARP_SMEM = W_RING * WS<TIn>::BYTES + W_NSTAGE * STAGE + 64;
 };
 
 __device__ __forceinline__ void w_mbar_init(u64* bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
 }
-__device__ __forceinline__ void w_load_tile(void* dst, const void* src, u64* bar) {
+__device__ __forceinline__ void w_load_tile(void* dst, const void* src, u32 bytes, u64* bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(W_BYTES)
+               "r"(bytes)
                : "memory");
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_addr(dst)),
-      "l"(src), "r"(W_BYTES), "r"(smem_addr(bar))
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
 }
 __device__ __forceinline__ void w_mbar_wait(u64* bar, u32 parity) {
@@ -401,29 +410,40 @@ __device__ __forceinline__ void w_mbar_wait(u64* bar, u32 parity) {
       : "memory");
 }
 
-// codes of one lane-row (8 input bytes) -> WR words
+// codes of one lane-row (8 input elements, LW words) -> WR words
 template <typename TIn, typename TC, bool kLut>
-__device__ __forceinline__ void wrow_codes(uint2 v, const u16* slut, const u16* glut,
-                                           u32 (&cw)[WF<TIn, TC>::WR]) {
+__device__ __forceinline__ void wrow_codes(const u32 (&v)[WF<TIn, TC>::LW], const u16* slut,
+                                           const u16* glut, u32 (&cw)[WF<TIn, TC>::WR]) {
   constexpr int WR = WF<TIn, TC>::WR;
   if (!kLut) {
-    cw[0] = v.x;
-    if (WR > 1) cw[WR - 1] = v.y;
+#pragma unroll
+    for (int i = 0; i < WR; ++i) cw[i] = v[i];  // TIn == TC
   } else {
-    constexpr int CR = WF<TIn, TC>::CR;
-    const u32 qw[2] = {v.x, v.y};
 #pragma unroll
     for (int i = 0; i < WR; ++i) cw[i] = 0;
 #pragma unroll
-    for (int j = 0; j < CR; ++j) {
-      const u32 raw = sizeof(TIn) == 1 ? (qw[j >> 2] >> ((j & 3) * 8)) & 0xffu
-                                       : (qw[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+    for (int j = 0; j < 8; ++j) {
+      const u32 raw = sizeof(TIn) == 1 ? (v[j >> 2] >> ((j & 3) * 8)) & 0xffu
+                                       : (v[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
       const u32 code = sizeof(TIn) == 1 ? (u32)slut[raw] : (u32)__ldg(glut + raw);
       if (sizeof(TC) == 1)
         cw[j >> 2] |= code << ((j & 3) * 8);
       else
         cw[j >> 1] |= code << ((j & 1) * 16);
     }
+  }
+}
+
+// one lane-row of the staged tile as LW words
+template <int LW>
+__device__ __forceinline__ void wrow_load(const u8* p, u32 (&v)[LW]) {
+  if (LW == 2) {
+    const uint2 x = *reinterpret_cast<const uint2*>(p);
+    v[0] = x.x;
+    v[LW - 1] = x.y;
+  } else {
+    const uint4 x = *reinterpret_cast<const uint4*>(p);
+    v[0] = x.x; v[1 % LW] = x.y; v[2 % LW] = x.z; v[3 % LW] = x.w;
   }
 }
 
@@ -546,20 +566,22 @@ __device__ __forceinline__ void wcount_tile(const u8* stage, u32 Z, u32 zoff, u6
 }
 
 template <typename TIn, typename TC, bool kLut>
-__global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_constant__ WLevelParams P) {
+__global__ void __launch_bounds__(W_NT, sizeof(TIn) == 1 ? W_MINB : 4)  // u16: smem allows 4 CTAs
+    wlevel_kernel(const __grid_constant__ WLevelParams P) {
   using S = WS<TIn>;
   using F = WF<TIn, TC>;
   constexpr int TILE = S::TILE, TPL1 = S::TPL1;
-  constexpr int CR = F::CR, RE = F::RE, ROWS = F::ROWS, WR = F::WR;
+  constexpr int CR = F::CR, RE = F::RE, ROWS = F::ROWS, WR = F::WR, LW = F::LW, LB = F::LB,
+                RB = F::RB, TB = S::BYTES;
   constexpr u32 SZ = sizeof(TC);
-  constexpr int NTILE_LOG = sizeof(TC) == 1 ? 11 : 10;  // next level's tile (input = codes)
+  constexpr int NTILE_LOG = 11;  // next level's tile: 2048 elements
   extern __shared__ __align__(128) u8 smem_raw[];
   u16* slut = reinterpret_cast<u16*>(smem_raw);  // 256 entries (u8 text + LUT)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   u8* wbase = smem_raw + 512 + warp * F::WARP_SMEM;
   u8* ring = wbase;
-  u8* stage0 = wbase + W_RING * W_BYTES;
-  u64* mbar = reinterpret_cast<u64*>(wbase + W_RING * W_BYTES + W_NSTAGE * F::STAGE);
+  u8* stage0 = wbase + W_RING * TB;
+  u64* mbar = reinterpret_cast<u64*>(wbase + W_RING * TB + W_NSTAGE * F::STAGE);
 
   if (kLut && sizeof(TIn) == 1) {
     for (int i = tid; i < 256; i += W_NT) slut[i] = P.lut[i];
@@ -578,7 +600,7 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
 #pragma unroll
     for (int i = 0; i < W_RING; ++i) {
       const u32 t = gw + i * nw;
-      if (t < nfull) w_load_tile(ring + i * W_BYTES, in + (u64)t * W_BYTES, &mbar[i]);
+      if (t < nfull) w_load_tile(ring + i * TB, in + (u64)t * TB, TB, &mbar[i]);
     }
   }
   __syncwarp();
@@ -591,7 +613,7 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
       if (scatter && lane == 0) w_bulk_commit();  // keep one bulk group per tile
       continue;
     }
-    const u8* tin = ring + slot * W_BYTES;
+    const u8* tin = ring + slot * TB;
     // ---- P1 (loads go out before the tile data is waited on) -----------------
     const u32 b = t / TPL1;
     const u32 tb = t - b * TPL1;
@@ -614,11 +636,32 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
       fcode = !kLut ? f : sizeof(TIn) == 1 ? (u32)slut[f] : (u32)__ldg(P.lut + f);
       lcode = !kLut ? l : sizeof(TIn) == 1 ? (u32)slut[l] : (u32)__ldg(P.lut + l);
     }
-    const u32 fkey = fcode >> P.shift_key;
-    if (scatter && fkey != (lcode >> P.shift_key)) {
+    const u32 fkey = fcode >> P.shift_key, lkey = lcode >> P.shift_key;
+    // two nodes (a node boundary inside the tile -- at deep levels of large
+    // alphabets most straddling tiles): keys are non-decreasing in the tile, so
+    // `split` = first element of the second node, found by binary search
+    u32 split = TILE;
+    // (u16 codes only: at u8 codes node boundaries inside a tile are rare and
+    // the extra code costs the single-node path registers)
+    constexpr bool kTwoSeg = sizeof(TC) == 2;
+    if (scatter && fkey != lkey && !kTwoSeg) split = 0;
+    if (kTwoSeg && scatter && fkey != lkey) {
+      u32 lo = 1, hi = TILE - 1;  // key(0) = fkey, key(TILE-1) = lkey
+      while (lo < hi) {
+        const u32 mid = (lo + hi) >> 1;
+        const u32 r = sizeof(TIn) == 1 ? (u32)tin[mid] : (u32)reinterpret_cast<const u16*>(tin)[mid];
+        const u32 c = !kLut ? r : sizeof(TIn) == 1 ? (u32)slut[r] : (u32)__ldg(P.lut + r);
+        if ((c >> P.shift_key) == fkey) lo = mid + 1; else hi = mid;
+      }
+      split = lo;
+      const u32 r = sizeof(TIn) == 1 ? (u32)tin[split] : (u32)reinterpret_cast<const u16*>(tin)[split];
+      const u32 c = !kLut ? r : sizeof(TIn) == 1 ? (u32)slut[r] : (u32)__ldg(P.lut + r);
+      if ((c >> P.shift_key) != lkey) split = 0;  // three or more nodes
+    }
+    if (scatter && split == 0) {
       __syncwarp();
       if (lane == 0 && t + W_RING * nw < nfull)
-        w_load_tile(ring + slot * W_BYTES, in + (u64)(t + W_RING * nw) * W_BYTES, &mbar[slot]);
+        w_load_tile(ring + slot * TB, in + (u64)(t + W_RING * nw) * TB, TB, &mbar[slot]);
       general_tile<TIn, TC, kLut>(P, t, slut);
       if (lane == 0) w_bulk_commit();  // keep one bulk group per tile
       continue;
@@ -631,20 +674,26 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
     u32 mrow[ROWS];
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
-      const uint2 v = *reinterpret_cast<const uint2*>(tin + r * 256 + lane * 8);
+      u32 v[LW];
+      wrow_load<LW>(tin + r * RB + lane * LB, v);
       if (kLut) {
         // level 0 through the LUT: the level bit is the TOP code bit, i.e.
         // `symbol >= thr` (codes are monotone in symbols) -- a SIMD compare
         // of the raw symbols, no table lookups in this pass
         if (sizeof(TIn) == 1) {
           const u32 t4 = P.thr * 0x01010101u;
-          const u32 y0 = __vcmpgeu4(v.x, t4) & 0x01010101u, y1 = __vcmpgeu4(v.y, t4) & 0x01010101u;
+          const u32 y0 = __vcmpgeu4(v[0], t4) & 0x01010101u, y1 = __vcmpgeu4(v[LW - 1], t4) & 0x01010101u;
           mrow[r] = P.thr > 0xffu ? 0u : ((y1 * 16u + y0) * 0x01020408u) >> 24;
         } else {
           const u32 t2 = P.thr * 0x00010001u;
-          const u32 y0 = __vcmpgeu2(v.x, t2) & 0x00010001u, y1 = __vcmpgeu2(v.y, t2) & 0x00010001u;
-          const u32 z = y1 * 4u + y0;  // bits 0, 16, 2, 18 -> elements 0, 1, 2, 3
-          mrow[r] = P.thr > 0xffffu ? 0u : (z | (z >> 15)) & 0xfu;
+          u32 mm = 0;
+#pragma unroll
+          for (int i = 0; i + 1 < LW; i += 2) {
+            const u32 y0 = __vcmpgeu2(v[i], t2) & 0x00010001u, y1 = __vcmpgeu2(v[i + 1], t2) & 0x00010001u;
+            const u32 z = y1 * 4u + y0;  // bits 0, 16, 2, 18 -> elements 0, 1, 2, 3
+            mm |= ((z | (z >> 15)) & 0xfu) << (2 * i);
+          }
+          mrow[r] = P.thr > 0xffffu ? 0u : mm;
         }
       } else {
         u32 cw[WR];
@@ -680,16 +729,8 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
 
     // ---- bit-vector words: each lane-row mask is CR bits at t0 + r*RE + lane*CR
 #pragma unroll
-    for (int r = 0; r < ROWS; ++r) {
-      if (CR == 8) {
-        reinterpret_cast<u8*>(P.words)[(t0 >> 3) + r * (RE / 8) + lane] = (u8)mrow[r];
-      } else {  // 4 bits: pair lanes into bytes
-        const u32 nb = __shfl_down_sync(FULLM, mrow[r], 1);
-        if (!(lane & 1))
-          reinterpret_cast<u8*>(P.words)[(t0 >> 3) + r * (RE / 8) + (lane >> 1)] =
-              (u8)(mrow[r] | (nb << 4));
-      }
-    }
+    for (int r = 0; r < ROWS; ++r)
+      reinterpret_cast<u8*>(P.words)[(t0 >> 3) + r * (RE / 8) + lane] = (u8)mrow[r];
 
     // ---- L2 entries: blocks start at lane-row boundaries (l2_bits >= 64) ------
     if ((1u << P.l2_log) >= (u32)RE) {  // at most one per row: lane r handles row r
@@ -751,28 +792,87 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
         __syncwarp();
       }
       const u32 tile_zeros = TILE - tile_ones;
+      // ones before `split` (segment A = [0, split), B = [split, TILE))
+      u32 onesA = tile_ones;
+      if (kTwoSeg && split < (u32)TILE) {
+        const u32 rs = split / RE, ls = (split % RE) / CR, js = split % CR;
+        u32 v = 0;
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r)
+          if ((u32)r == rs) v = r1[r] + __popc(mrow[r] & ((1u << js) - 1u));
+        onesA = __shfl_sync(FULLM, v, ls);
+      }
+      const u32 zerosA = split - onesA;
       const NodeEnt* ne = P.nodes + fkey;
       const u64 zdst = (u64)__ldg(&ne->zero_base) + (t0 - P1);
       const u64 odst = (u64)__ldg(&ne->one_base) + P1;
       const u32 zoff = (u32)((zdst * SZ) & 15);
-      const u32 ooff = ((zoff + tile_zeros * SZ + 15) & ~15u) + (u32)((odst * SZ) & 15);
-      const bool zlive = tile_zeros && zdst < P.m_next;
-      const bool olive = tile_ones && odst < P.m_next;
+      const u32 ooff = ((zoff + zerosA * SZ + 15) & ~15u) + (u32)((odst * SZ) & 15);
+      const bool zlive = zerosA && zdst < P.m_next;
+      const bool olive = onesA && odst < P.m_next;
+      // segment B runs (empty when the tile lies in one node)
+      const u32 onesB = tile_ones - onesA, zerosB = tile_zeros - zerosA;
+      u64 zdstB = 0, odstB = 0;
+      u32 zoffB = 0, ooffB = 0;
+      if (kTwoSeg && split < (u32)TILE) {
+        const NodeEnt* nb = P.nodes + lkey;
+        zdstB = (u64)__ldg(&nb->zero_base) + (t0 + split - P1 - onesA);
+        odstB = (u64)__ldg(&nb->one_base) + P1 + onesA;
+        zoffB = ((ooff + onesA * SZ + 15) & ~15u) + (u32)((zdstB * SZ) & 15);
+        ooffB = ((zoffB + zerosB * SZ + 15) & ~15u) + (u32)((odstB * SZ) & 15);
+      }
+      const bool zliveB = zerosB && zdstB < P.m_next;
+      const bool oliveB = onesB && odstB < P.m_next;
+      if (!kTwoSeg || split == (u32)TILE) {  // one node (the common case): two runs
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+          u32 v[LW];
+          wrow_load<LW>(tin + r * RB + lane * LB, v);
+          u32 cw[WR];
+          if (!kLut) wrow_codes<TIn, TC, kLut>(v, slut, P.lut, cw);
+          const u32 m = mrow[r];
+          u32 oa = sbase + ooff + r1[r] * SZ;
+          u32 za = sbase + zoff + ((u32)(r * RE + lane * CR) - r1[r]) * SZ;
+#pragma unroll
+          for (int j = 0; j < CR; ++j) {
+            // st.shared.u8/u16 keep the low bits: no masking of the element
+            u32 val;
+            if (kLut) {  // map each raw symbol as it is stored
+              const u32 raw = sizeof(TIn) == 1 ? (v[j >> 2] >> ((j & 3) * 8)) & 0xffu
+                                               : (v[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+              val = sizeof(TIn) == 1 ? (u32)slut[raw] : (u32)__ldg(P.lut + raw);
+            } else {
+              val = sizeof(TC) == 1 ? cw[j >> 2] >> ((j & 3) * 8) : cw[j >> 1] >> ((j & 1) * 16);
+            }
+            if (m & (1u << j)) {
+              st_shared<TC>(oa, val);
+              oa += SZ;
+            } else {
+              st_shared<TC>(za, val);
+              za += SZ;
+            }
+          }
+        }
+      } else {  // two nodes: four runs
 #pragma unroll
       for (int r = 0; r < ROWS; ++r) {
-        const uint2 v = *reinterpret_cast<const uint2*>(tin + r * 256 + lane * 8);
+        u32 v[LW];
+        wrow_load<LW>(tin + r * RB + lane * LB, v);
         u32 cw[WR];
         if (!kLut) wrow_codes<TIn, TC, kLut>(v, slut, P.lut, cw);
         const u32 m = mrow[r];
-        u32 oa = sbase + ooff + r1[r] * SZ;
-        u32 za = sbase + zoff + ((u32)(r * RE + lane * CR) - r1[r]) * SZ;
-#pragma unroll
-        for (int j = 0; j < CR; ++j) {
+        const u32 e0 = (u32)(r * RE + lane * CR);
+        const bool inB = e0 >= split;  // whole lane-row in segment B
+        u32 oa = inB ? sbase + ooffB + (r1[r] - onesA) * SZ : sbase + ooff + r1[r] * SZ;
+        u32 za = inB ? sbase + zoffB + ((e0 - split) - (r1[r] - onesA)) * SZ
+                     : sbase + zoff + (e0 - r1[r]) * SZ;
+        const u32 jsw = (!inB && e0 + CR > split) ? split - e0 : (u32)CR;  // switch to B inside
+        auto element = [&](int j) {
           // st.shared.u8/u16 keep the low bits: no masking of the element
           u32 val;
           if (kLut) {  // map each raw symbol as it is stored
-            const u32 raw = sizeof(TIn) == 1 ? ((j < 4 ? v.x : v.y) >> ((j & 3) * 8)) & 0xffu
-                                             : ((j < 2 ? v.x : v.y) >> ((j & 1) * 16)) & 0xffffu;
+            const u32 raw = sizeof(TIn) == 1 ? (v[j >> 2] >> ((j & 3) * 8)) & 0xffu
+                                             : (v[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
             val = sizeof(TIn) == 1 ? (u32)slut[raw] : (u32)__ldg(P.lut + raw);
           } else {
             val = sizeof(TC) == 1 ? cw[j >> 2] >> ((j & 3) * 8) : cw[j >> 1] >> ((j & 1) * 16);
@@ -784,21 +884,36 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
             st_shared<TC>(za, val);
             za += SZ;
           }
+        };
+        if (jsw == (u32)CR) {
+#pragma unroll
+          for (int j = 0; j < CR; ++j) element(j);
+        } else {  // the one lane-row holding the node boundary
+#pragma unroll
+          for (int j = 0; j < CR; ++j) {
+            if ((u32)j == jsw) {
+              oa = sbase + ooffB;
+              za = sbase + zoffB;
+            }
+            element(j);
+          }
         }
+      }
       }
       w_fence_proxy();
       __syncwarp();
       // the input slot is free: the tile three ahead streams into it
       if (lane == 0 && t + W_RING * nw < nfull)
-        w_load_tile(ring + slot * W_BYTES, in + (u64)(t + W_RING * nw) * W_BYTES, &mbar[slot]);
+        w_load_tile(ring + slot * TB, in + (u64)(t + W_RING * nw) * TB, TB, &mbar[slot]);
       u8* gout = reinterpret_cast<u8*>(P.out);
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        const bool live = rr ? olive : zlive;
+      for (int rr = 0; rr < 4; ++rr) {
+        if (rr >= 2 && (!kTwoSeg || split == (u32)TILE)) break;
+        const bool live = rr == 0 ? zlive : rr == 1 ? olive : rr == 2 ? zliveB : oliveB;
         if (!live) continue;
-        const u32 cnt = rr ? tile_ones : tile_zeros;
-        const u64 dst = rr ? odst : zdst;
-        const u32 soff = rr ? ooff : zoff;
+        const u32 cnt = rr == 0 ? zerosA : rr == 1 ? onesA : rr == 2 ? zerosB : onesB;
+        const u64 dst = rr == 0 ? zdst : rr == 1 ? odst : rr == 2 ? zdstB : odstB;
+        const u32 soff = rr == 0 ? zoff : rr == 1 ? ooff : rr == 2 ? zoffB : ooffB;
         const u32 bytes = cnt * SZ;
         const u64 db = dst * SZ;
         u32 head = (u32)((16 - (db & 15)) & 15);
@@ -814,13 +929,16 @@ __global__ void __launch_bounds__(W_NT, W_MINB) wlevel_kernel(const __grid_const
       }
       // next level's ones of both runs per next-level tile (<= 3 per run) and
       // L1 block, in one pass over the staged tile
-      wcount_tile<TC>(stage, zlive ? tile_zeros : 0u, zoff, zdst, olive ? tile_ones : 0u, ooff, odst,
+      wcount_tile<TC>(stage, zlive ? zerosA : 0u, zoff, zdst, olive ? onesA : 0u, ooff, odst,
                       P.shift_bit - 1, NTILE_LOG, P.next_tile_counts, P.next_l1_counts, lane);
+      if (kTwoSeg && split < (u32)TILE)
+        wcount_tile<TC>(stage, zliveB ? zerosB : 0u, zoffB, zdstB, oliveB ? onesB : 0u, ooffB, odstB,
+                        P.shift_bit - 1, NTILE_LOG, P.next_tile_counts, P.next_l1_counts, lane);
       if (lane == 0) w_bulk_commit();  // one bulk group per scattering fast tile
     } else {
       __syncwarp();
       if (lane == 0 && t + W_RING * nw < nfull)
-        w_load_tile(ring + slot * W_BYTES, in + (u64)(t + W_RING * nw) * W_BYTES, &mbar[slot]);
+        w_load_tile(ring + slot * TB, in + (u64)(t + W_RING * nw) * TB, TB, &mbar[slot]);
     }
   }
   if (scatter && lane == 0) w_bulk_wait_all();
@@ -837,7 +955,8 @@ __global__ void __launch_bounds__(256) wlast_kernel(const __grid_constant__ WLev
   using S = WS<TIn>;
   constexpr int TILE = S::TILE, TPL1 = S::TPL1;
   constexpr int CH = 16 / (int)sizeof(TIn);   // elements per 16-byte chunk
-  constexpr int E = 4 * CH;                   // elements per lane (64 | 32)
+  constexpr int K = S::K;                     // 16-byte chunks per lane
+  constexpr int E = K * CH;                   // elements per lane: 64
   constexpr int WPC = CH * (int)sizeof(TC) / 4;
   __shared__ u16 slut[kLut && sizeof(TIn) == 1 ? 256 : 1];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -861,11 +980,11 @@ __global__ void __launch_bounds__(256) wlast_kernel(const __grid_constant__ WLev
       if (j < tb) pre += __ldg(P.tile_counts + b * TPL1 + j);
     }
     const u64 l1v = __ldg(P.l1 + b);
-    const u8* base = in + t0 * sizeof(TIn) + lane * 64;
+    const u8* base = in + t0 * sizeof(TIn) + lane * (K * 16);
     const u32 e0 = (u32)lane * E;  // first element of this lane in the tile
     u64 m = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < K; ++k) {
       const u32 e = e0 + k * CH;
       uint4 q;
       if (e + CH <= valid) {
@@ -946,12 +1065,12 @@ __global__ void __launch_bounds__(256) wcount0_kernel(const TIn* __restrict__ te
   const u32 t4 = sizeof(TIn) == 1 ? thr * 0x01010101u : thr * 0x00010001u;
   const bool none = thr > (sizeof(TIn) == 1 ? 0xffu : 0xffffu);
   for (u32 t = blockIdx.x * 8 + (threadIdx.x >> 5); t < ntiles; t += gridDim.x * 8) {
-    uint4 q[W_K];
+    uint4 q[S::K];
     wload<TIn>(reinterpret_cast<const u8*>(text), n, t, lane, q);
     const u64 t0 = (u64)t * S::TILE;
     u32 cnt = 0;
 #pragma unroll
-    for (int k = 0; k < W_K; ++k) {
+    for (int k = 0; k < S::K; ++k) {
       const u32 e = (u32)(k * 32 + lane) * CH;
       const u32 w4[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
       u32 c = 0;

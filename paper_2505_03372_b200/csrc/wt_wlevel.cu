@@ -52,10 +52,14 @@ constexpr unsigned FULLM = 0xffffffffu;
 // a warp tile is 2048 elements for both input widths (2 KiB of u8 / 4 KiB
 // of u16), so per-tile costs are amortized alike and every level's tile
 // counts have the same granularity
+#ifndef WT_U8_TILE
+#define WT_U8_TILE 4096
+#endif
 template <typename TIn>
 struct WS {
   static constexpr int CH = 16 / (int)sizeof(TIn);          // elements per 16-byte chunk
-  static constexpr int TILE = 2048;                         // elements per warp tile
+  static constexpr int TILE = sizeof(TIn) == 1 ? WT_U8_TILE : 2048;  // elements per warp tile
+  static constexpr int LOG = TILE == 4096 ? 12 : 11;
   static constexpr int BYTES = TILE * (int)sizeof(TIn);     // 2048 | 4096
   static constexpr int K = BYTES / 512;                     // 16-byte chunks per lane (4 | 8)
   static constexpr int TPL1 = kL1Bits / TILE;               // 32 tiles per L1 block
@@ -201,7 +205,7 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
   using S = WS<TIn>;
   constexpr int CH = S::CH, TILE = S::TILE, TPL1 = S::TPL1;
   constexpr int WPC = CH * (int)sizeof(TC) / 4;
-  constexpr int NTILE_LOG = 11;  // next level's tile: 2048 elements
+  constexpr int NTILE_LOG = WS<TC>::LOG;  // next level's tile (its input = codes)
   const int lane = threadIdx.x & 31;
   const bool scatter = P.out != nullptr;
   const u8* in = reinterpret_cast<const u8*>(P.in);
@@ -218,7 +222,7 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
     const u32 tb = t - b * TPL1;  // tiles of the block before this one
     u32 pre = 0;
 #pragma unroll
-    for (int r = 0; r < TPL1 / 32; ++r) {
+    for (int r = 0; r < (TPL1 + 31) / 32; ++r) {
       const u32 j = r * 32 + lane;
       if (j < tb) pre += __ldg(P.tile_counts + b * TPL1 + j);
     }
@@ -566,7 +570,7 @@ __device__ __forceinline__ void wcount_tile(const u8* stage, u32 Z, u32 zoff, u6
 }
 
 template <typename TIn, typename TC, bool kLut>
-__global__ void __launch_bounds__(W_NT, sizeof(TIn) == 1 ? W_MINB : 4)  // u16: smem allows 4 CTAs
+__global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 4 KiB tiles: smem allows 4 CTAs
     wlevel_kernel(const __grid_constant__ WLevelParams P) {
   using S = WS<TIn>;
   using F = WF<TIn, TC>;
@@ -574,7 +578,7 @@ __global__ void __launch_bounds__(W_NT, sizeof(TIn) == 1 ? W_MINB : 4)  // u16: 
   constexpr int CR = F::CR, RE = F::RE, ROWS = F::ROWS, WR = F::WR, LW = F::LW, LB = F::LB,
                 RB = F::RB, TB = S::BYTES;
   constexpr u32 SZ = sizeof(TC);
-  constexpr int NTILE_LOG = 11;  // next level's tile: 2048 elements
+  constexpr int NTILE_LOG = WS<TC>::LOG;  // next level's tile (its input = codes)
   extern __shared__ __align__(128) u8 smem_raw[];
   u16* slut = reinterpret_cast<u16*>(smem_raw);  // 256 entries (u8 text + LUT)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -619,7 +623,7 @@ __global__ void __launch_bounds__(W_NT, sizeof(TIn) == 1 ? W_MINB : 4)  // u16: 
     const u32 tb = t - b * TPL1;
     u32 pre = 0;
 #pragma unroll
-    for (int r = 0; r < TPL1 / 32; ++r) {
+    for (int r = 0; r < (TPL1 + 31) / 32; ++r) {
       const u32 j = r * 32 + lane;
       if (j < tb) pre += __ldg(P.tile_counts + b * TPL1 + j);
     }
@@ -975,14 +979,17 @@ __global__ void __launch_bounds__(256) wlast_kernel(const __grid_constant__ WLev
     const u32 b = t / TPL1, tb = t - b * TPL1;
     u32 pre = 0;
 #pragma unroll
-    for (int r = 0; r < TPL1 / 32; ++r) {
+    for (int r = 0; r < (TPL1 + 31) / 32; ++r) {
       const u32 j = r * 32 + lane;
       if (j < tb) pre += __ldg(P.tile_counts + b * TPL1 + j);
     }
     const u64 l1v = __ldg(P.l1 + b);
     const u8* base = in + t0 * sizeof(TIn) + lane * (K * 16);
     const u32 e0 = (u32)lane * E;  // first element of this lane in the tile
-    u64 m = 0;
+    constexpr int NW = E / 64;     // bit-vector words per lane (1 | 2)
+    u64 m[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) m[w] = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const u32 e = e0 + k * CH;
@@ -999,12 +1006,17 @@ __global__ void __launch_bounds__(256) wlast_kernel(const __grid_constant__ WLev
       wcodes<TIn, TC, kLut, WPC>(q, slut, P.lut, cw);
       u32 mk = wmask<TC, WPC>(cw, P.shift_bit);
       if (e + CH > valid) mk &= e >= valid ? 0u : (1u << (valid - e)) - 1u;
-      m |= (u64)mk << (k * CH);
+      m[(k * CH) / 64] |= (u64)mk << ((k * CH) % 64);
     }
 #pragma unroll
     for (int d = 16; d; d >>= 1) pre += __shfl_xor_sync(FULLM, pre, d);
     const u64 P1 = l1v + pre;
-    const u32 c = __popcll(m);
+    u32 wc[NW], c = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      wc[w] = __popcll(m[w]);
+      c += wc[w];
+    }
     u32 inc = c;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -1013,17 +1025,16 @@ __global__ void __launch_bounds__(256) wlast_kernel(const __grid_constant__ WLev
     }
     const u32 tile_ones = __shfl_sync(FULLM, inc, 31);
     const u32 pl = inc - c;  // ones of the tile before this lane
-    if (e0 < ((valid + 63u) & ~63u)) {
-      if (E == 64)
-        P.words[(t0 >> 6) + lane] = m;
-      else
-        reinterpret_cast<u32*>(P.words)[(t0 >> 5) + lane] = (u32)m;
+    u32 before = pl;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const u32 ew = e0 + 64 * w;
+      const u64 g = t0 + ew;
+      if (ew < ((valid + 63u) & ~63u)) P.words[(g >> 6)] = m[w];
+      if (ew < valid && (g & l2m) == 0) P.l2[g >> P.l2_log] = (u16)(P1 + before - l1v);
+      before += wc[w];
     }
-    const u64 g = t0 + e0;
-    if (e0 < valid && (g & l2m) == 0) P.l2[g >> P.l2_log] = (u16)(P1 + pl - l1v);
     // select samples (rankselect.py:509-532)
-    const u32 lv = e0 >= valid ? 0u : min((u32)E, valid - e0);
-    const u64 vmask = lv >= 64 ? ~0ull : ((1ull << lv) - 1);
 #pragma unroll
     for (int kind = 0; kind < 2; ++kind) {
       const bool ones = kind == 0;
@@ -1031,16 +1042,31 @@ __global__ void __launch_bounds__(256) wlast_kernel(const __grid_constant__ WLev
       const u32 cnt = ones ? tile_ones : valid - tile_ones;
       const u64 q0 = wnext_multiple(sb, P.rate, P.rate_log);
       if (q0 > sb + cnt) continue;
-      const u64 mk = ones ? m : (~m & vmask);
+      const u32 lvalid = e0 >= valid ? 0u : min((u32)E, valid - e0);
+      const u32 lc = ones ? c : lvalid - c;
       const u32 lp = ones ? pl : e0 - pl;
-      const u32 lc = __popcll(mk);
       u64* out = ones ? P.ones : P.zeros;
       const u64 cap = ones ? P.ones_cap : P.zeros_cap;
       for (u64 qo = q0; qo <= sb + cnt; qo += P.rate) {
-        const u32 tt = (u32)(qo - sb);
+        u32 tt = (u32)(qo - sb);
         if (lp < tt && tt <= lp + lc) {
+          tt -= lp;
+          u32 pos = e0;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            const u32 ew = e0 + 64 * w;
+            const u32 wv = ew >= valid ? 0u : min(64u, valid - ew);
+            const u64 wm = ones ? m[w] : (~m[w] & (wv >= 64 ? ~0ull : ((1ull << wv) - 1)));
+            const u32 pc = __popcll(wm);
+            if (tt > 0 && tt <= pc) {
+              pos = ew + select_in_word64(wm, tt);
+              tt = 0;
+            } else if (tt > 0) {
+              tt -= pc;
+            }
+          }
           const u64 sidx = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
-          if (sidx < cap) out[sidx] = g + select_in_word64(mk, tt - lp);
+          if (sidx < cap) out[sidx] = t0 + pos;
         }
       }
     }

@@ -602,8 +602,7 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       TRY(S.get(&p, (uint64_t)P.sizes[2] * P.code_bytes + 16));
       cur[1] = p;
     }
-    static const bool cta_levels = getenv("WT_LEVEL_CTA") != nullptr;  // A/B: old CTA-tile kernel
-    if (!cta_levels) {
+    {
       // K2w: warp tiles; per-tile and per-L1-block ones counts of each level
       // come from the previous level's scatter (level 0: a counting pass)
       uint64_t max_tiles = 1, max_l1 = 1;
@@ -670,59 +669,6 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       }
       // (the query-side layouts run after the last level: overlapping them
       // with the next level's kernel on a side stream measured slower)
-    } else {
-    uint64_t max_tiles = 1;
-    for (uint32_t l = 0; l < P.L; ++l)
-      max_tiles = std::max<uint64_t>(
-          max_tiles, level_tiles((uint64_t)P.sizes[l], l == 0 ? sym_bytes : P.code_bytes));
-    u32* counts[2];
-    u64* prefix;
-    TRY(S.get(&counts[0], max_tiles + 4));
-    TRY(S.get(&counts[1], max_tiles + 4));
-    TRY(S.get(&prefix, max_tiles + 1));
-    if (P.L && P.sizes[0]) {
-      const uint32_t tiles0 = level_tiles((uint64_t)P.sizes[0], sym_bytes);
-      CU(cudaMemsetAsync(counts[0], 0, (size_t)(tiles0 + 4) * 4, st));
-      CU(launch_level0_counts(dtext, n, sym_bytes, dlut, P.L - 1, counts[0], st));
-    }
-    int ci = 0;
-    for (uint32_t l = 0; l < P.L; ++l) {
-      const uint64_t m = (uint64_t)P.sizes[l];
-      CU(cudaEventRecord(lev[l], st));
-      if (m == 0) continue;
-      const int in_bytes = l == 0 ? sym_bytes : P.code_bytes;
-      const uint32_t tiles = level_tiles(m, in_bytes);
-      LevelHost& h = t->lv[l];
-      CU(launch_tile_scan(counts[ci], tiles, level_tiles_per_l1(in_bytes), prefix, h.l1,
-                          h.meta.n_l1, totals + l, st));
-      LevelParams lp{};
-      lp.in = l == 0 ? dtext : cur[(l - 1) & 1];
-      lp.out = l + 1 < P.L ? cur[l & 1] : nullptr;
-      lp.m = m;
-      lp.m_next = l + 1 < P.L ? (uint64_t)P.sizes[l + 1] : 0;
-      if (lp.out && lp.m_next == 0) lp.out = nullptr;
-      if (lp.out) {
-        const uint32_t ntiles_next = level_tiles(lp.m_next, P.code_bytes);
-        CU(cudaMemsetAsync(counts[ci ^ 1], 0, (size_t)(ntiles_next + 4) * 4, st));
-      }
-      lp.words = t->words + (P.offsets[l] >> 6);
-      lp.l2 = h.l2;
-      lp.ones = h.ones;
-      lp.zeros = h.zeros;
-      lp.ones_cap = m / sample_rate;
-      lp.zeros_cap = m / sample_rate;
-      lp.nodes = t->nodes + P.node_off[l];
-      lp.lut = l == 0 ? dlut : nullptr;
-      lp.prefix = prefix;
-      lp.next_counts = counts[ci ^ 1];
-      lp.shift_bit = P.L - 1 - l;
-      lp.shift_key = P.L - l;
-      lp.l2_log = l2_log;
-      lp.rate_log = rate_log_of(sample_rate);
-      lp.rate = sample_rate;
-      CU(launch_level(lp, in_bytes, P.code_bytes, l == 0 && dlut != nullptr, st));
-      ci ^= 1;
-    }
     }
     TRY(launch_qlayouts(t, totals, st));
     tr.mark("levels launched");

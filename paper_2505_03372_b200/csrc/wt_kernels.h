@@ -4,39 +4,6 @@
 
 namespace wt {
 
-// K2 parameters for one level (wt_level.cu)
-struct LevelParams {
-  const void* in;        // level input: text (level 0) or the partitioned codes
-  void* out;             // next level's codes (nullptr at the last level)
-  u64 m, m_next;         // level_sizes[l], level_sizes[l+1]
-  u64* words;            // region start
-  u16* l2;
-  u64* ones;
-  u64* zeros;
-  u64 ones_cap, zeros_cap;
-  const NodeEnt* nodes;  // 2^l entries keyed by the l-bit code prefix
-  const u16* lut;        // level 0: raw symbol -> code (nullptr: identity)
-  const u64* prefix;     // exclusive ones prefix per tile of this level (+ total)
-  u32* next_counts;      // ones of level l+1 per tile of level l+1 (atomics)
-  u32 shift_bit;         // L-1-l
-  u32 shift_key;         // L-l
-  u32 l2_log;
-  int rate_log;          // log2(rate) when rate is a power of two, else -1
-  u64 rate;
-};
-
-cudaError_t launch_level(const LevelParams& p, int in_bytes, int code_bytes, bool lut,
-                         cudaStream_t st);
-// tiles of a level whose input elements are `in_bytes` wide
-u32 level_tiles(u64 m, int in_bytes);
-// ones per tile of level 0 (reads the text through the symbol -> code LUT)
-cudaError_t launch_level0_counts(const void* text, u64 n, int in_bytes, const u16* lut,
-                                 u32 shift_bit, u32* counts, cudaStream_t st);
-// exclusive scan of per-tile counts -> prefix[0..tiles], l1[] and total
-cudaError_t launch_tile_scan(const u32* counts, u32 tiles, int tiles_per_l1, u64* prefix,
-                             u64* l1, u64 n_l1, u64* total, cudaStream_t st);
-int level_tiles_per_l1(int in_bytes);
-
 // K2w parameters (wt_wlevel.cu): warp-granular tiles of 2 KB of input
 struct WLevelParams {
   const void* in;          // level input: text (level 0) or the partitioned codes

@@ -122,6 +122,27 @@ def traffic(rep, queries_per_launch):
     print(json.dumps(out, indent=1))
 
 
+def traffic_csv(path, queries_per_launch):
+    """dram bytes per query from a `--metrics dram__bytes_*` launch CSV taken
+    at the bench's own batch size (one launch per kernel)."""
+    with open(path) as f:
+        lines = [l for l in f if not l.startswith("==")]
+    rows = list(csv.reader(io.StringIO("".join(lines))))
+    hdr = rows[0]
+    ix = {h: i for i, h in enumerate(hdr)}
+    acc = {}
+    for r in rows[1:]:
+        m = re.match(r"void (\w+)", r[ix["Kernel Name"]]) or re.match(r"(\w+)", r[ix["Kernel Name"]])
+        name = m.group(1).split("::")[-1]
+        metric = r[ix["Metric Name"]]
+        if metric.startswith("dram__bytes"):
+            acc.setdefault(name, 0.0)
+            acc[name] += to_bytes(r[ix["Metric Value"]], r[ix["Metric Unit"]])
+    out = {k: {"dram_bytes": v, "queries": queries_per_launch,
+               "dram_bytes_per_query": v / queries_per_launch} for k, v in acc.items()}
+    print(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
     cmd, path = sys.argv[1], sys.argv[2]
     if cmd == "report":
@@ -130,5 +151,7 @@ if __name__ == "__main__":
         launches(path)
     elif cmd == "traffic":
         traffic(path, int(sys.argv[3]) if len(sys.argv) > 3 else 1_000_000)
+    elif cmd == "traffic_csv":
+        traffic_csv(path, int(sys.argv[3]) if len(sys.argv) > 3 else 33_333_334)
     else:
         raise SystemExit(__doc__)

@@ -315,8 +315,8 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
     while ((1u << sym_bits) < T.sigma) ++sym_bits;
   const u32 bits_per_sym = 16 - sym_bits;
   const u64 arg_span = kind == 2 ? S.max_occ : T.n + 1;  // args in [0, arg_span)
-  u32 arg_shift = 0;
-  while ((arg_span >> arg_shift) > (1ull << bits_per_sym)) ++arg_shift;
+  u32 arg_shift = 0;  // the largest argument must fit in bits_per_sym bits
+  while (((arg_span - 1) >> arg_shift) >= (1ull << bits_per_sym)) ++arg_shift;
   const u32 nb = 1u << 16;
   cudaError_t e = cudaMemsetAsync(S.hist, 0, nb * 4, st);
   if (e != cudaSuccess) return e;

@@ -128,3 +128,15 @@ def test_device_query_sort_keeps_answers_and_errors(W, chunk):
                                       C.byref(badi), None))
     assert badi.value == -1
     assert np.array_equal(out.cpu().numpy(), W.select_batch(t, ssym, ks))
+
+
+def test_device_query_sort_largest_argument(W):
+    """n + 1 = 2^20 + 1 puts rank(c, n) exactly on the top of the 16-bit key
+    range: the key must still land in one of the 65536 buckets."""
+    text = np.random.default_rng(31).integers(0, 256, 1 << 20, dtype=np.uint8)
+    t = W.construct(text)
+    syms = t.alphabet.sorted_symbols.astype(np.int64)
+    pos = np.full(len(syms), len(text), np.int64)
+    want = np.array([(text == s).sum() for s in syms], np.int64)
+    assert np.array_equal(W.rank_batch(t, syms, pos, sort=True), want)
+    assert np.array_equal(W.rank_batch(t, syms, pos), want)

@@ -140,3 +140,22 @@ def test_device_query_sort_largest_argument(W):
     want = np.array([(text == s).sum() for s in syms], np.int64)
     assert np.array_equal(W.rank_batch(t, syms, pos, sort=True), want)
     assert np.array_equal(W.rank_batch(t, syms, pos), want)
+
+
+def test_nccl_replicate_world1(W):
+    """The NCCL path of wt_tree_replicate (dlopen'ed NCCL, header + grouped
+    broadcasts) at world size 1 -- the only size a one-GPU box can run; the
+    multi-rank host logic is covered by tests/test_parallel_cpu.py."""
+    import ctypes as C
+    from paper_2505_03372_b200 import _lib
+    text = np.random.default_rng(41).integers(0, 256, 1 << 20, dtype=np.uint8)
+    t = W.construct(text)
+    uid = (C.c_uint8 * 128)()
+    _lib.check(_lib.lib.wt_nccl_unique_id(uid), "wt_nccl_unique_id")
+    out = C.c_void_p()
+    ms = C.c_float(-1)
+    _lib.check(_lib.lib.wt_tree_replicate(t.handle, uid, 0, 1, _lib.current_device(), C.byref(out),
+                                          C.byref(ms)), "wt_tree_replicate")
+    assert out.value is None and ms.value >= 0  # the root keeps its own tree
+    pos = np.random.default_rng(42).integers(0, len(text), 1000)
+    assert np.array_equal(W.access_batch(t, pos), text[pos])

@@ -451,12 +451,16 @@ __device__ __forceinline__ void wrow_load(const u8* p, u32 (&v)[LW]) {
   }
 }
 
+// No "memory" clobber: the scatter's loads (ring rows, LUT) may be hoisted
+// above these stores -- they read other buffers.  The stores stay ordered
+// among themselves and before w_fence_proxy() (volatile asm, which clobbers
+// memory) that publishes the staging buffer.
 template <typename TC>
 __device__ __forceinline__ void st_shared(u32 addr, u32 v) {
   if (sizeof(TC) == 1)
-    asm("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v));
   else
-    asm("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v));
 }
 
 // SWAR count of bit `sh` of every code in a 16-byte chunk
@@ -587,8 +591,14 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
   u8* stage0 = wbase + W_RING * TB;
   u64* mbar = reinterpret_cast<u64*>(wbase + W_RING * TB + W_NSTAGE * F::STAGE);
 
+  // the scatter's copy of the LUT: code-sized entries at a static address, so
+  // a lookup is one LDS [raw + imm] after one PRMT extracting the byte
+  __shared__ TC slutc[kLut && sizeof(TIn) == 1 ? 256 : 1];
   if (kLut && sizeof(TIn) == 1) {
-    for (int i = tid; i < 256; i += W_NT) slut[i] = P.lut[i];
+    for (int i = tid; i < 256; i += W_NT) {
+      slut[i] = P.lut[i];
+      slutc[i] = (TC)P.lut[i];
+    }
     __syncthreads();
   }
   const u32 ntiles = (u32)((P.m + TILE - 1) / TILE);
@@ -828,26 +838,40 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
       const bool zliveB = zerosB && zdstB < P.m_next;
       const bool oliveB = onesB && odstB < P.m_next;
       if (!kTwoSeg || split == (u32)TILE) {  // one node (the common case): two runs
+        // loads stay ahead of the stores in program order (ptxas keeps shared
+        // loads behind earlier shared stores it cannot disambiguate): the next
+        // lane-row and this row's LUT lookups are issued before the stores
+        // (u8 input only: at u16 the extra row of registers spills)
+        constexpr bool kPre = sizeof(TIn) == 1;
+        u32 vn[LW];
+        if (kPre) wrow_load<LW>(tin + lane * LB, vn);
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
           u32 v[LW];
-          wrow_load<LW>(tin + r * RB + lane * LB, v);
+          if (kPre) {
+#pragma unroll
+            for (int i = 0; i < LW; ++i) v[i] = vn[i];
+            if (r + 1 < ROWS) wrow_load<LW>(tin + (r + 1) * RB + lane * LB, vn);
+          } else {
+            wrow_load<LW>(tin + r * RB + lane * LB, v);
+          }
           u32 cw[WR];
           if (!kLut) wrow_codes<TIn, TC, kLut>(v, slut, P.lut, cw);
+          u32 lv[CR];
+          if (kLut) {  // map each raw symbol
+#pragma unroll
+            for (int j = 0; j < CR; ++j)
+              lv[j] = sizeof(TIn) == 1 ? (u32)slutc[__byte_perm(v[j >> 2], 0u, 0x4440u + (j & 3))]
+                                       : (u32)__ldg(P.lut + ((v[j >> 1] >> ((j & 1) * 16)) & 0xffffu));
+          }
           const u32 m = mrow[r];
           u32 oa = sbase + ooff + r1[r] * SZ;
           u32 za = sbase + zoff + ((u32)(r * RE + lane * CR) - r1[r]) * SZ;
 #pragma unroll
           for (int j = 0; j < CR; ++j) {
             // st.shared.u8/u16 keep the low bits: no masking of the element
-            u32 val;
-            if (kLut) {  // map each raw symbol as it is stored
-              const u32 raw = sizeof(TIn) == 1 ? (v[j >> 2] >> ((j & 3) * 8)) & 0xffu
-                                               : (v[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
-              val = sizeof(TIn) == 1 ? (u32)slut[raw] : (u32)__ldg(P.lut + raw);
-            } else {
-              val = sizeof(TC) == 1 ? cw[j >> 2] >> ((j & 3) * 8) : cw[j >> 1] >> ((j & 1) * 16);
-            }
+            const u32 val = kLut ? lv[j]
+                                 : sizeof(TC) == 1 ? cw[j >> 2] >> ((j & 3) * 8) : cw[j >> 1] >> ((j & 1) * 16);
             if (m & (1u << j)) {
               st_shared<TC>(oa, val);
               oa += SZ;
@@ -875,9 +899,8 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
           // st.shared.u8/u16 keep the low bits: no masking of the element
           u32 val;
           if (kLut) {  // map each raw symbol as it is stored
-            const u32 raw = sizeof(TIn) == 1 ? (v[j >> 2] >> ((j & 3) * 8)) & 0xffu
-                                             : (v[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
-            val = sizeof(TIn) == 1 ? (u32)slut[raw] : (u32)__ldg(P.lut + raw);
+            val = sizeof(TIn) == 1 ? (u32)slutc[__byte_perm(v[j >> 2], 0u, 0x4440u + (j & 3))]
+                                   : (u32)__ldg(P.lut + ((v[j >> 1] >> ((j & 1) * 16)) & 0xffffu));
           } else {
             val = sizeof(TC) == 1 ? cw[j >> 2] >> ((j & 3) * 8) : cw[j >> 1] >> ((j & 1) * 16);
           }

@@ -485,7 +485,18 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
     u64* dhist;
     TRY(S.get(&dhist, nb));
     CU(cudaMemsetAsync(dhist, 0, nb * 8, st));
-    CU(launch_histogram(dtext, n, sym_bytes, dhist, sm_count(device), st));
+    // Large u8 texts: K1 also keeps the histogram of every L1 block, from
+    // which level 0's L1 counts follow once the plan fixes the top-bit
+    // threshold, and level 0 runs in block mode (no counting pass over the
+    // text).  Enough blocks to keep every resident warp of the level kernel
+    // busy are required: a warp walks whole blocks.
+    const uint64_t n_blk = (n + 65535) >> 16;
+    u32* dbh = nullptr;
+    // (WT_BLOCK_MODE=0|1 forces it off / on: the parity tests run both)
+    const char* bm = getenv("WT_BLOCK_MODE");
+    if (sym_bytes == 1 && (bm ? bm[0] == '1' : n_blk >= 2 * wlevel_warp_slots(sm_count(device))))
+      TRY(S.get(&dbh, n_blk * 256));
+    CU(launch_histogram(dtext, n, sym_bytes, dhist, sm_count(device), st, dbh));
     std::vector<uint64_t> hraw(nb);
     CU(cudaMemcpyAsync(hraw.data(), dhist, nb * 8, cudaMemcpyDeviceToHost, st));
     tr.mark("histogram launched");
@@ -623,9 +634,13 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
           thr = P.symbols[i];
           break;
         }
+      const bool block_mode = dbh && P.L >= 2;
       if (P.L && P.sizes[0]) {
         CU(cudaMemsetAsync(l1cnt[0], 0, (t->lv[0].meta.n_l1 + 4) * 4, st));
-        CU(launch_wcount0(dtext, n, sym_bytes, thr, tcnt[0], l1cnt[0], sm_count(device), st));
+        if (block_mode)
+          CU(launch_block_l1(dbh, n_blk, thr, l1cnt[0], st));
+        else
+          CU(launch_wcount0(dtext, n, sym_bytes, thr, tcnt[0], l1cnt[0], sm_count(device), st));
       }
       int ci = 0;
       for (uint32_t l = 0; l < P.L; ++l) {
@@ -655,7 +670,7 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
         wp.nodes = t->nodes + P.node_off[l];
         wp.lut = l == 0 ? dlut : nullptr;
         wp.l1 = h.l1;
-        wp.tile_counts = tcnt[ci];
+        wp.tile_counts = l == 0 && block_mode ? nullptr : tcnt[ci];
         wp.next_tile_counts = tcnt[ci ^ 1];
         wp.next_l1_counts = l1cnt[ci ^ 1];
         wp.thr = thr;

@@ -46,6 +46,71 @@ __global__ void __launch_bounds__(H_NT) hist8_kernel(const u8* __restrict__ text
   }
 }
 
+// u8 with per-block histograms (the level-0 block mode of the level kernel):
+// a CTA takes whole 65536-symbol L1 blocks, each warp an 8 KiB slice of the
+// block into its shared sub-histogram; thread i then folds bin i of the eight
+// sub-histograms, writes it to block_hist[block][i] and keeps a running total
+// for the text histogram.
+constexpr int HB_BLOCK = 65536;
+__global__ void __launch_bounds__(H_NT) hist8_blocks_kernel(const u8* __restrict__ text, u64 n,
+                                                            u64* __restrict__ hist,
+                                                            u32* __restrict__ block_hist) {
+  __shared__ u32 sh[H_NT / 32][256];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < (H_NT / 32) * 256; i += H_NT) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  u32* mine = sh[warp];
+  constexpr int SLICE = HB_BLOCK / (H_NT / 32);  // 8192 bytes per warp
+  const u64 nblk = (n + HB_BLOCK - 1) / HB_BLOCK;
+  u64 total = 0;
+  for (u64 c = blockIdx.x; c < nblk; c += gridDim.x) {
+    const u64 s0 = c * HB_BLOCK + (u64)warp * SLICE;
+    const u8* p = text + s0;
+    if (s0 + SLICE <= n) {
+#pragma unroll 4
+      for (int k = 0; k < SLICE / 512; ++k) {
+        const uint4 q = ld_stream16(p + (k * 32 + lane) * 16);
+        const u32 w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) atomicAdd(&mine[(w[i] >> (8 * b)) & 0xff], 1u);
+        }
+      }
+    } else if (s0 < n) {
+      for (u64 i = s0 + lane; i < n; i += 32) atomicAdd(&mine[text[i]], 1u);
+    }
+    __syncthreads();
+    u32 v = 0;
+#pragma unroll
+    for (int w = 0; w < H_NT / 32; ++w) {
+      v += sh[w][tid];
+      sh[w][tid] = 0;
+    }
+    block_hist[c * 256 + tid] = v;
+    total += v;
+    __syncthreads();
+  }
+  if (total) atomicAdd(&hist[tid], total);
+}
+
+// ones of every L1 block for level 0 (symbols >= thr): a warp per block
+__global__ void __launch_bounds__(256) block_l1_kernel(const u32* __restrict__ block_hist, u64 nblk,
+                                                       u32 thr, u32* __restrict__ l1_counts) {
+  const int lane = threadIdx.x & 31;
+  for (u64 c = (u64)blockIdx.x * 8 + (threadIdx.x >> 5); c < nblk; c += (u64)gridDim.x * 8) {
+    u32 s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const u32 b = j * 32 + lane;
+      if (b >= thr) s += __ldg(block_hist + c * 256 + b);
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+    if (lane == 0) l1_counts[c] = s;
+  }
+}
+
 // u16: CTAs work in pairs over the same chunks of the text; CTA 2k counts
 // symbols < 32768 and CTA 2k+1 the rest, each into 32768 u32 shared bins
 // (128 KB, one CTA per SM).  The pair reads each chunk at about the same
@@ -93,8 +158,14 @@ __global__ void __launch_bounds__(H_NT) first_outside_kernel(const void* __restr
 }
 
 cudaError_t launch_histogram(const void* text, u64 n, int sym_bytes, u64* hist, int sms,
-                             cudaStream_t st) {
+                             cudaStream_t st, u32* block_hist) {
   if (n == 0) return cudaSuccess;
+  if (sym_bytes == 1 && block_hist) {
+    const u64 nblk = (n + HB_BLOCK - 1) / HB_BLOCK;
+    const u64 blocks = nblk < (u64)sms * 8 ? nblk : (u64)sms * 8;
+    hist8_blocks_kernel<<<(unsigned)blocks, H_NT, 0, st>>>((const u8*)text, n, hist, block_hist);
+    return cudaGetLastError();
+  }
   const u64 work = sym_bytes == 1 ? (n >> 4) : (n >> 3);
   u64 blocks = (work + H_NT - 1) / H_NT;
   const u64 cap = (u64)sms * 8;
@@ -123,6 +194,15 @@ cudaError_t launch_first_outside(const void* text, u64 n, int sym_bytes, const u
   const u64 cap = (u64)sms * 8;
   if (blocks > cap) blocks = cap;
   first_outside_kernel<<<(unsigned)blocks, H_NT, 0, st>>>(text, n, sym_bytes, member, best);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_l1(const u32* block_hist, u64 n_blocks, u32 thr, u32* l1_counts,
+                            cudaStream_t st) {
+  if (n_blocks == 0) return cudaSuccess;
+  u64 blocks = (n_blocks + 7) / 8;
+  if (blocks > 65535) blocks = 65535;
+  block_l1_kernel<<<(unsigned)blocks, 256, 0, st>>>(block_hist, n_blocks, thr, l1_counts);
   return cudaGetLastError();
 }
 

@@ -17,7 +17,7 @@ struct WLevelParams {
   const NodeEnt* nodes;    // 2^l entries keyed by the l-bit code prefix
   const u16* lut;          // level 0: raw symbol -> code (nullptr: identity)
   const u64* l1;           // this level's L1 directory (ones before each 65536-bit block)
-  const u32* tile_counts;  // ones per warp tile of this level
+  const u32* tile_counts;  // ones per warp tile of this level (nullptr: block mode, level 0)
   u32* next_tile_counts;   // ones of level l+1 per warp tile of level l+1 (atomics)
   u32* next_l1_counts;     // ones of level l+1 per L1 block (atomics)
   u32 thr;                 // level 0 with a LUT: smallest symbol whose code has the top bit
@@ -30,6 +30,12 @@ struct WLevelParams {
 cudaError_t launch_wlevel(const WLevelParams& p, int in_bytes, int code_bytes, bool lut, int sms,
                           cudaStream_t st);
 u32 wlevel_tiles(u64 m, int in_bytes);
+// resident warps of the u8 level kernel on the device (block-mode threshold)
+u64 wlevel_warp_slots(int sms);
+// level 0 of a u8 text in block mode (WLevelParams::tile_counts == nullptr):
+// per-L1-block ones (symbols >= thr) from the per-block histograms K1 wrote
+cudaError_t launch_block_l1(const u32* block_hist, u64 n_blocks, u32 thr, u32* l1_counts,
+                            cudaStream_t st);
 // ones per warp tile of level 0: text symbols >= thr (the top code bit)
 cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, u32 thr, u32* tile_counts,
                            u32* l1_counts, int sms, cudaStream_t st);
@@ -37,8 +43,10 @@ cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, u32 thr, u32* 
 cudaError_t launch_l1_scan(const u32* counts, u64 n_l1, u64* l1, u64* total, cudaStream_t st);
 
 // K1: raw-symbol histogram (wt_hist.cu); hist must be zeroed (u64[256|65536])
+// block_hist (u8 only, may be null): also the 256-bin histogram of every
+// 65536-symbol L1 block, u32[n_blocks][256]
 cudaError_t launch_histogram(const void* text, u64 n, int sym_bytes, u64* hist, int sms,
-                             cudaStream_t st);
+                             cudaStream_t st, u32* block_hist = nullptr);
 // first text position whose raw symbol has member[sym] == 0; *best preset to ~0
 cudaError_t launch_first_outside(const void* text, u64 n, int sym_bytes, const u8* member,
                                  u64* best, int sms, cudaStream_t st);

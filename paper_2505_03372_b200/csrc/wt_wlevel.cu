@@ -201,7 +201,7 @@ __device__ __forceinline__ u64 wnext_multiple(u64 o, u64 rate, int rate_log) {
 // spanning several nodes): loads from global memory, element-by-element
 // destination stores, per-element next-level counts.
 template <typename TIn, typename TC, bool kLut>
-__device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u16* slut) {
+__device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u16* slut, u64 p1_in) {
   using S = WS<TIn>;
   constexpr int CH = S::CH, TILE = S::TILE, TPL1 = S::TPL1;
   constexpr int WPC = CH * (int)sizeof(TC) / 4;
@@ -217,19 +217,21 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
   for (int k = 0; k < S::K; ++k) wcodes<TIn, TC, kLut, WPC>(q[k], slut, P.lut, cw[k]);
     const u64 t0 = (u64)t * TILE;
     const u32 valid = (u32)min((u64)TILE, P.m - t0);
-    // ---- P1: ones before the tile ------------------------------------------
+    // ---- P1: ones before the tile (block mode: the caller's running count) ---
     const u32 b = t / TPL1;
     const u32 tb = t - b * TPL1;  // tiles of the block before this one
     u32 pre = 0;
+    if (p1_in == ~0ull) {
 #pragma unroll
-    for (int r = 0; r < (TPL1 + 31) / 32; ++r) {
-      const u32 j = r * 32 + lane;
-      if (j < tb) pre += __ldg(P.tile_counts + b * TPL1 + j);
+      for (int r = 0; r < (TPL1 + 31) / 32; ++r) {
+        const u32 j = r * 32 + lane;
+        if (j < tb) pre += __ldg(P.tile_counts + b * TPL1 + j);
+      }
+#pragma unroll
+      for (int d = 16; d; d >>= 1) pre += __shfl_xor_sync(FULLM, pre, d);
     }
-#pragma unroll
-    for (int d = 16; d; d >>= 1) pre += __shfl_xor_sync(FULLM, pre, d);
     const u64 l1v = __ldg(P.l1 + b);
-    const u64 P1 = l1v + pre;
+    const u64 P1 = p1_in == ~0ull ? l1v + pre : p1_in;
 
     // ---- 1. codes, masks, in-tile scan ---------------------------------------
     u32 msk[S::K];
@@ -604,6 +606,14 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
   const u32 ntiles = (u32)((P.m + TILE - 1) / TILE);
   const u32 nfull = (u32)(P.m / TILE);
   const u32 gw = blockIdx.x * W_WARPS + warp, nw = gridDim.x * W_WARPS;
+  // Block mode (level 0 of a large u8 text, tile_counts == nullptr): a warp
+  // takes whole L1 blocks and walks their tiles in order, so P1 is the L1
+  // entry plus the warp's own running count -- no per-tile counting pass.
+  const bool blockm = P.tile_counts == nullptr;
+  auto tile_at = [&](u32 i) -> u32 {
+    return blockm ? (gw + (i / TPL1) * nw) * TPL1 + i % TPL1 : gw + i * nw;
+  };
+  u32 run = 0;  // block mode: ones of the block's tiles before this one
   const bool scatter = P.out != nullptr;
   const u8* in = reinterpret_cast<const u8*>(P.in);
 
@@ -613,17 +623,19 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < W_RING; ++i) {
-      const u32 t = gw + i * nw;
+      const u32 t = tile_at(i);
       if (t < nfull) w_load_tile(ring + i * TB, in + (u64)t * TB, TB, &mbar[i]);
     }
   }
   __syncwarp();
 
   u32 it = 0;
-  for (u32 t = gw; t < ntiles; t += nw, ++it) {
+  for (u32 t = tile_at(0); t < ntiles; t = tile_at(++it)) {
     const u32 slot = it % W_RING;
+    const u32 tnext = tile_at(it + W_RING);  // the tile this ring slot streams next
+    if (blockm && t % TPL1 == 0) run = 0;
     if (t >= nfull) {  // the partial last tile
-      general_tile<TIn, TC, kLut>(P, t, slut);
+      general_tile<TIn, TC, kLut>(P, t, slut, blockm ? __ldg(P.l1 + t / TPL1) + run : ~0ull);
       if (scatter && lane == 0) w_bulk_commit();  // keep one bulk group per tile
       continue;
     }
@@ -632,10 +644,12 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
     const u32 b = t / TPL1;
     const u32 tb = t - b * TPL1;
     u32 pre = 0;
+    if (!blockm) {
 #pragma unroll
-    for (int r = 0; r < (TPL1 + 31) / 32; ++r) {
-      const u32 j = r * 32 + lane;
-      if (j < tb) pre += __ldg(P.tile_counts + b * TPL1 + j);
+      for (int r = 0; r < (TPL1 + 31) / 32; ++r) {
+        const u32 j = r * 32 + lane;
+        if (j < tb) pre += __ldg(P.tile_counts + b * TPL1 + j);
+      }
     }
     const u64 l1v = __ldg(P.l1 + b);
     const u64 t0 = (u64)t * TILE;
@@ -674,15 +688,17 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
     }
     if (scatter && split == 0) {
       __syncwarp();
-      if (lane == 0 && t + W_RING * nw < nfull)
-        w_load_tile(ring + slot * TB, in + (u64)(t + W_RING * nw) * TB, TB, &mbar[slot]);
-      general_tile<TIn, TC, kLut>(P, t, slut);
+      if (lane == 0 && tnext < nfull)
+        w_load_tile(ring + slot * TB, in + (u64)tnext * TB, TB, &mbar[slot]);
+      general_tile<TIn, TC, kLut>(P, t, slut, blockm ? l1v + run : ~0ull);
       if (lane == 0) w_bulk_commit();  // keep one bulk group per tile
       continue;
     }
+    if (!blockm) {
 #pragma unroll
-    for (int d = 16; d; d >>= 1) pre += __shfl_xor_sync(FULLM, pre, d);
-    const u64 P1 = l1v + pre;
+      for (int d = 16; d; d >>= 1) pre += __shfl_xor_sync(FULLM, pre, d);
+    }
+    const u64 P1 = l1v + (blockm ? run : pre);
 
     // ---- pass 1: masks and counts per row ------------------------------------
     u32 mrow[ROWS];
@@ -740,6 +756,7 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
       r1[r] += tile_ones;
       tile_ones += rtot[r];
     }
+    run += tile_ones;
 
     // ---- bit-vector words: each lane-row mask is CR bits at t0 + r*RE + lane*CR
 #pragma unroll
@@ -930,8 +947,8 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
       w_fence_proxy();
       __syncwarp();
       // the input slot is free: the tile three ahead streams into it
-      if (lane == 0 && t + W_RING * nw < nfull)
-        w_load_tile(ring + slot * TB, in + (u64)(t + W_RING * nw) * TB, TB, &mbar[slot]);
+      if (lane == 0 && tnext < nfull)
+        w_load_tile(ring + slot * TB, in + (u64)tnext * TB, TB, &mbar[slot]);
       u8* gout = reinterpret_cast<u8*>(P.out);
 #pragma unroll
       for (int rr = 0; rr < 4; ++rr) {
@@ -964,8 +981,8 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
       if (lane == 0) w_bulk_commit();  // one bulk group per scattering fast tile
     } else {
       __syncwarp();
-      if (lane == 0 && t + W_RING * nw < nfull)
-        w_load_tile(ring + slot * TB, in + (u64)(t + W_RING * nw) * TB, TB, &mbar[slot]);
+      if (lane == 0 && tnext < nfull)
+        w_load_tile(ring + slot * TB, in + (u64)tnext * TB, TB, &mbar[slot]);
     }
   }
   if (scatter && lane == 0) w_bulk_wait_all();
@@ -1213,7 +1230,9 @@ cudaError_t launch_w(const WLevelParams& p, int sms, cudaStream_t st) {
     wlast_kernel<TIn, TC, kLut><<<(unsigned)blocks, 256, 0, st>>>(p);
     return cudaGetLastError();
   }
-  const u64 need = (tiles + W_WARPS - 1) / W_WARPS;
+  // block mode: one warp per L1 block is all the parallelism there is
+  const u64 units = p.tile_counts ? tiles : (tiles + WS<TIn>::TPL1 - 1) / WS<TIn>::TPL1;
+  const u64 need = (units + W_WARPS - 1) / W_WARPS;
   const u64 cap = (u64)sms * per_sm;
   kern<<<(unsigned)(need < cap ? need : cap), W_NT, smem, st>>>(p);
   return cudaGetLastError();
@@ -1248,6 +1267,18 @@ cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, u32 thr, u32* 
 cudaError_t launch_l1_scan(const u32* counts, u64 n_l1, u64* l1, u64* total, cudaStream_t st) {
   l1_scan_kernel<<<1, 1024, 0, st>>>(counts, n_l1, l1, total);
   return cudaGetLastError();
+}
+
+u64 wlevel_warp_slots(int sms) {
+  int per_sm = 1;
+  const size_t smem = 512 + (size_t)W_WARPS * WF<u8, u8>::WARP_SMEM;
+  auto kern = wlevel_kernel<u8, u8, false>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W_NT, smem) != cudaSuccess) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  return (u64)sms * (per_sm < 1 ? 1 : per_sm) * W_WARPS;
 }
 
 u32 wlevel_tiles(u64 m, int in_bytes) {

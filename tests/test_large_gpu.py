@@ -159,3 +159,27 @@ def test_nccl_replicate_world1(W):
     assert out.value is None and ms.value >= 0  # the root keeps its own tree
     pos = np.random.default_rng(42).integers(0, len(text), 1000)
     assert np.array_equal(W.access_batch(t, pos), text[pos])
+
+
+BLOCK_MODE = {
+    "u8_s256_full": LARGE["u8_s256_full"],
+    "u8_s256_partial": LARGE["u8_s256_partial"],
+    "u8_s200_lut": LARGE["u8_s200_lut"],
+    "dna": LARGE["dna"],
+    "u8_skewed": LARGE["u8_skewed"],
+    "one_block": lambda: np.random.default_rng(7).integers(0, 256, 65536, dtype=np.uint8),
+    "under_one_block": lambda: np.random.default_rng(8).integers(0, 9, 40000, dtype=np.uint8),
+    "blocks_plus_one": lambda: np.random.default_rng(9).integers(0, 256, 3 * 65536 + 1, dtype=np.uint8),
+}
+
+
+@pytest.mark.parametrize("name", sorted(BLOCK_MODE))
+def test_level0_block_mode(W, name, monkeypatch):
+    """Level 0 of a u8 text in block mode (a warp walks whole L1 blocks, P1 from
+    the per-block histograms of K1) -- the default for large texts, forced here
+    at test sizes -- gives the oracle's tree."""
+    monkeypatch.setenv("WT_BLOCK_MODE", "1")
+    text = BLOCK_MODE[name]()
+    t = W.construct(text)
+    assert_same_structure(t, O.build(text))
+    _check_queries(W, t, text, t.alphabet.sorted_symbols, m=5000)

@@ -896,7 +896,6 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
       QuerySortScratch Q{};
       TRY(S.get(&Q.hist, 65536));
       TRY(S.get(&Q.bucket_of, slice));
-      TRY(S.get(&Q.ids_mapped, slice));
       TRY(S.get(&Q.sorted_args, slice));
       TRY(S.get(&Q.perm, slice));
       Q.max_occ = max_occ(t);
@@ -929,9 +928,8 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
   if (chunk == 0) chunk = 1ull << 22;
   if (chunk > m) chunk = m;
   const bool sorted = (flags & WT_F_SORT) != 0;
-  // per slot: ids, args, out [+ sort scratch: buckets, bucket_of, mapped ids,
-  // sorted ids, sorted args, perm]
-  const size_t sort_bytes = sorted ? 65536 * 4 + chunk * (4 + 8 + 8 + 8 + 4) + 64 : 0;
+  // per slot: ids, args, out [+ sort scratch: buckets, sorted args, bucket_of, perm]
+  const size_t sort_bytes = sorted ? 65536 * 4 + chunk * (8 + 4 + 4) + 64 : 0;
   const size_t need = chunk * (16 + out_elem) + 64 + sort_bytes;
   for (int i = 0; i < 3; ++i) {
     if (!t->qstream[i]) CU(cudaStreamCreateWithFlags(&t->qstream[i], cudaStreamNonBlocking));
@@ -982,9 +980,7 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
       u8* sp = (u8*)(((uintptr_t)(d_out + chunk * out_elem) + 15) & ~(uintptr_t)15);
       QuerySortScratch Q{};
       Q.hist = (u32*)sp;
-      Q.ids_mapped = (i64*)(sp + 65536 * 4);
-      Q.sorted_ids = Q.ids_mapped + chunk;
-      Q.sorted_args = Q.sorted_ids + chunk;
+      Q.sorted_args = (i64*)(sp + 65536 * 4);
       Q.bucket_of = (u32*)(Q.sorted_args + chunk);
       Q.perm = Q.bucket_of + chunk;
       Q.max_occ = max_occ(t);

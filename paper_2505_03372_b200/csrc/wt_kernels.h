@@ -63,9 +63,7 @@ cudaError_t launch_query(const TreeDev& T, int kind, int out_kind, bool validate
 // query kernel on the sorted batch writing results back in query order
 struct QuerySortScratch {
   u32* hist;        // 65536 bucket counts / cursors
-  u32* bucket_of;   // m
-  i64* ids_mapped;  // m (minimal ids)
-  i64* sorted_ids;  // unused (ids ride in sorted_args' top 16 bits)
+  u32* bucket_of;   // m (the minimal id is the bucket's top bits)
   i64* sorted_args; // m: argument | id << 48
   u32* perm;        // m
   u64 max_occ;      // largest symbol count (select ordinals are below it)

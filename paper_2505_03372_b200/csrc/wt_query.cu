@@ -207,7 +207,6 @@ __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__
                                                          const i64* __restrict__ args, u64 m,
                                                          bool validate, u32 bits_per_sym,
                                                          u32 arg_shift, u32* __restrict__ bucket_of,
-                                                         i64* __restrict__ ids_out,
                                                          u32* __restrict__ hist, u64 base,
                                                          u64* __restrict__ bad) {
   const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
@@ -233,8 +232,8 @@ __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__
       else ok = a >= 1 && (i64)a <= __ldg(T.cum + c + 1) - __ldg(T.cum + c);
     }
     const u64 sub = kind == 1 ? a : a - 1;
+    // (the bucket's top bits are the minimal id: the scatter recovers it)
     bucket = ok ? (c << bits_per_sym) | (u32)(sub >> arg_shift) : 0u;
-    ids_out[i] = c;
   }
   if (!ok) atomicMin(bad, base + i);
   bucket_of[i] = bucket;
@@ -288,18 +287,19 @@ __global__ void __launch_bounds__(1024) qsort_scan_kernel(u32* __restrict__ hist
 
 // the sorted batch: (argument | id << 48) and the query index -- 12 bytes
 // of scattered writes per query (ids ride in the argument's top bits:
-// positions / ordinals stay below 2^48)
+// positions / ordinals stay below 2^48; the id is the bucket's top bits)
 __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restrict__ bucket_of,
-                                                             const i64* __restrict__ ids_in,
+                                                             bool with_id, u32 bits_per_sym,
                                                              const i64* __restrict__ args, u64 m,
                                                              u32* __restrict__ cursor,
                                                              i64* __restrict__ sargs,
                                                              u32* __restrict__ perm) {
   const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
   if (i >= m) return;
-  const u32 slot = atomicAdd(cursor + bucket_of[i], 1u);
+  const u32 b = bucket_of[i];
+  const u32 slot = atomicAdd(cursor + b, 1u);
   const u64 a = (u64)args[i] & ((1ull << 48) - 1);
-  sargs[slot] = (i64)(ids_in ? a | ((u64)ids_in[i] << 48) : a);
+  sargs[slot] = (i64)(with_id ? a | ((u64)(b >> bits_per_sym) << 48) : a);
   perm[slot] = (u32)i;
 }
 
@@ -321,10 +321,10 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   cudaError_t e = cudaMemsetAsync(S.hist, 0, nb * 4, st);
   if (e != cudaSuccess) return e;
   qsort_key_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(T, kind, ids, args, m, validate, bits_per_sym,
-                                                      arg_shift, S.bucket_of, S.ids_mapped, S.hist,
+                                                      arg_shift, S.bucket_of, S.hist,
                                                       base, bad);
   qsort_scan_kernel<<<1, 1024, 0, st>>>(S.hist, nb);
-  qsort_scatter_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(S.bucket_of, kind ? S.ids_mapped : nullptr,
+  qsort_scatter_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(S.bucket_of, kind != 0, bits_per_sym,
                                                           args, m, S.hist, S.sorted_args, S.perm);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -897,7 +897,12 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
       TRY(S.get(&Q.hist, 65536));
       TRY(S.get(&Q.bucket_of, slice));
       TRY(S.get(&Q.sorted_args, slice));
-      TRY(S.get(&Q.perm, slice));
+      TRY(S.get(&Q.slot_of, slice));
+      {
+        u8* r;
+        TRY(S.get(&r, slice * out_elem));
+        Q.res = r;
+      }
       Q.max_occ = max_occ(t);
       for (uint64_t a = 0; a < m; a += slice) {
         const uint64_t cnt = std::min(slice, m - a);
@@ -928,8 +933,9 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
   if (chunk == 0) chunk = 1ull << 22;
   if (chunk > m) chunk = m;
   const bool sorted = (flags & WT_F_SORT) != 0;
-  // per slot: ids, args, out [+ sort scratch: buckets, sorted args, bucket_of, perm]
-  const size_t sort_bytes = sorted ? 65536 * 4 + chunk * (8 + 4 + 4) + 64 : 0;
+  // per slot: ids, args, out [+ sort scratch: buckets, slot_of, sorted args,
+  // bucket_of, sorted-order results; each 16-byte aligned]
+  const size_t sort_bytes = sorted ? 65536 * 4 + chunk * (4 + 8 + 4 + out_elem) + 5 * 16 : 0;
   const size_t need = chunk * (16 + out_elem) + 64 + sort_bytes;
   for (int i = 0; i < 3; ++i) {
     if (!t->qstream[i]) CU(cudaStreamCreateWithFlags(&t->qstream[i], cudaStreamNonBlocking));
@@ -979,10 +985,16 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
     } else if (e == cudaSuccess) {
       u8* sp = (u8*)(((uintptr_t)(d_out + chunk * out_elem) + 15) & ~(uintptr_t)15);
       QuerySortScratch Q{};
-      Q.hist = (u32*)sp;
-      Q.sorted_args = (i64*)(sp + 65536 * 4);
-      Q.bucket_of = (u32*)(Q.sorted_args + chunk);
-      Q.perm = Q.bucket_of + chunk;
+      auto take = [&](size_t bytes) {
+        u8* p = sp;
+        sp = (u8*)(((uintptr_t)(sp + bytes) + 15) & ~(uintptr_t)15);
+        return p;
+      };
+      Q.hist = (u32*)take(65536 * 4);
+      Q.slot_of = (u32*)take(chunk * 4);
+      Q.sorted_args = (i64*)take(chunk * 8);
+      Q.bucket_of = (u32*)take(chunk * 4);
+      Q.res = take(chunk * out_elem);
       Q.max_occ = max_occ(t);
       e = launch_query_sorted(t->dev, kind, out_kind, validate, d_ids, d_args, d_out, cnt,
                               t->rate_log, a, t->bad, Q, sk);

@@ -54,10 +54,10 @@ cudaError_t launch_first_outside(const void* text, u64 n, int sym_bytes, const u
 // Q kernels (wt_query.cu)
 // kind 0/1/2 = access/rank/select; out_kind (access): 1|2 = symbol bytes, 8 = int64 id;
 // validate: ids are original symbols, invalid queries -> atomicMin(bad, base + i)
-// perm (optional): query q writes result slot perm[q] (sorted batches)
+// packed: arguments are the device sort's (argument | id << 48), clamped, unvalidated
 cudaError_t launch_query(const TreeDev& T, int kind, int out_kind, bool validate, const i64* ids,
                          const i64* args, void* out, u64 m, int rate_log, u64 base, u64* bad,
-                         cudaStream_t st, const u32* perm = nullptr);
+                         cudaStream_t st, bool packed = false);
 
 // device sort_queries_by_symbol: counting sort into 65536 buckets, then the
 // query kernel on the sorted batch writing results back in query order
@@ -65,7 +65,8 @@ struct QuerySortScratch {
   u32* hist;        // 65536 bucket counts / cursors
   u32* bucket_of;   // m (the minimal id is the bucket's top bits)
   i64* sorted_args; // m: argument | id << 48
-  u32* perm;        // m
+  u32* slot_of;     // m: sorted slot of each query (query order)
+  void* res;        // m results in sorted order (out_kind bytes each)
   u64 max_occ;      // largest symbol count (select ordinals are below it)
 };
 cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool validate,

@@ -38,12 +38,12 @@ __global__ void __launch_bounds__(Q_NT) access_kernel(const __grid_constant__ Tr
                                                       const i64* __restrict__ pos,
                                                       void* __restrict__ out, u64 m, u64 base,
                                                       u64* __restrict__ bad,
-                                                      const u32* __restrict__ perm) {
+                                                      bool packed) {
   const u64 q = (u64)blockIdx.x * Q_NT + threadIdx.x;
   if (q >= m) return;
-  const u64 i = perm ? (u64)__ldg(perm + q) : q;  // result slot (sorted batches)
+  const u64 i = q;
   u64 p = (u64)pos[q];
-  if (perm) p = min(p & ((1ull << 48) - 1), T.n - 1);  // sorted batch: clamped in range
+  if (packed) p = min(p & ((1ull << 48) - 1), T.n - 1);  // sorted batch: clamped in range
   if (kValidate && p >= T.n) {  // negative positions wrap to huge values
     atomicMin(bad, base + i);
     return;
@@ -92,13 +92,13 @@ __global__ void __launch_bounds__(Q_NT) rank_kernel(const __grid_constant__ Tree
                                                     const i64* __restrict__ pos,
                                                     i64* __restrict__ out, u64 m, u64 base,
                                                     u64* __restrict__ bad,
-                                                    const u32* __restrict__ perm) {
+                                                    bool packed) {
   const u64 q = (u64)blockIdx.x * Q_NT + threadIdx.x;
   if (q >= m) return;
-  const u64 i = perm ? (u64)__ldg(perm + q) : q;
+  const u64 i = q;
   u32 c;
   u64 p;
-  if (perm) {  // sorted batch: packed (position | id << 48), clamped in range
+  if (packed) {  // sorted batch: packed (position | id << 48), clamped in range
     qsort_unpack(pos[q], c, p);
     p = min(p, T.n);
   } else {
@@ -127,13 +127,13 @@ __global__ void __launch_bounds__(Q_NT) select_kernel(const __grid_constant__ Tr
                                                       const i64* __restrict__ ks,
                                                       i64* __restrict__ out, u64 m, int rate_log,
                                                       u64 base, u64* __restrict__ bad,
-                                                      const u32* __restrict__ perm) {
+                                                      bool packed) {
   const u64 q = (u64)blockIdx.x * Q_NT + threadIdx.x;
   if (q >= m) return;
-  const u64 i = perm ? (u64)__ldg(perm + q) : q;
+  const u64 i = q;
   u32 c;
   i64 k;
-  if (perm) {  // sorted batch: packed (ordinal | id << 48), clamped in range
+  if (packed) {  // sorted batch: packed (ordinal | id << 48), clamped in range
     u64 a;
     qsort_unpack(ks[q], c, a);
     const i64 occ = __ldg(T.cum + c + 1) - __ldg(T.cum + c);
@@ -160,37 +160,37 @@ __global__ void __launch_bounds__(Q_NT) select_kernel(const __grid_constant__ Tr
 
 template <bool V>
 static void launch_q(const TreeDev& T, int kind, int out_kind, const i64* ids, const i64* args,
-                     void* out, u64 m, int rate_log, u64 base, u64* bad, const u32* perm,
+                     void* out, u64 m, int rate_log, u64 base, u64* bad, bool packed,
                      unsigned blocks, cudaStream_t st) {
   switch (kind) {
     case 0:
       if (out_kind == 8)
-        access_kernel<8, V><<<blocks, Q_NT, 0, st>>>(T, args, out, m, base, bad, perm);
+        access_kernel<8, V><<<blocks, Q_NT, 0, st>>>(T, args, out, m, base, bad, packed);
       else if (out_kind == 1)
-        access_kernel<1, V><<<blocks, Q_NT, 0, st>>>(T, args, out, m, base, bad, perm);
+        access_kernel<1, V><<<blocks, Q_NT, 0, st>>>(T, args, out, m, base, bad, packed);
       else
-        access_kernel<2, V><<<blocks, Q_NT, 0, st>>>(T, args, out, m, base, bad, perm);
+        access_kernel<2, V><<<blocks, Q_NT, 0, st>>>(T, args, out, m, base, bad, packed);
       break;
     case 1:
-      rank_kernel<V><<<blocks, Q_NT, 0, st>>>(T, ids, args, (i64*)out, m, base, bad, perm);
+      rank_kernel<V><<<blocks, Q_NT, 0, st>>>(T, ids, args, (i64*)out, m, base, bad, packed);
       break;
     default:
-      select_kernel<V><<<blocks, Q_NT, 0, st>>>(T, ids, args, (i64*)out, m, rate_log, base, bad, perm);
+      select_kernel<V><<<blocks, Q_NT, 0, st>>>(T, ids, args, (i64*)out, m, rate_log, base, bad, packed);
       break;
   }
 }
 
 cudaError_t launch_query(const TreeDev& T, int kind, int out_kind, bool validate, const i64* ids,
                          const i64* args, void* out, u64 m, int rate_log, u64 base, u64* bad,
-                         cudaStream_t st, const u32* perm) {
+                         cudaStream_t st, bool packed) {
   if (m == 0) return cudaSuccess;
   if (kind < 0 || kind > 2) return cudaErrorInvalidValue;
   const u64 blocks = (m + Q_NT - 1) / Q_NT;
   if (blocks > 0x7fffffffull) return cudaErrorInvalidValue;
   if (validate)
-    launch_q<true>(T, kind, out_kind, ids, args, out, m, rate_log, base, bad, perm, (unsigned)blocks, st);
+    launch_q<true>(T, kind, out_kind, ids, args, out, m, rate_log, base, bad, packed, (unsigned)blocks, st);
   else
-    launch_q<false>(T, kind, out_kind, ids, args, out, m, rate_log, base, bad, perm, (unsigned)blocks, st);
+    launch_q<false>(T, kind, out_kind, ids, args, out, m, rate_log, base, bad, packed, (unsigned)blocks, st);
   return cudaGetLastError();
 }
 
@@ -199,8 +199,9 @@ cudaError_t launch_query(const TreeDev& T, int kind, int out_kind, bool validate
 // a counting sort into at most 65,536 buckets -- (symbol id, coarse
 // position / ordinal) for rank / select, coarse position for access -- so
 // queries that walk the same nodes and nearby lines run side by side.
-// Results go back to query order through the permutation (the kernels'
-// `perm`).  Validation happens here, before anything runs (batch.py:112-148).
+// The query kernel writes results in sorted order; qunsort_kernel gathers
+// them back into query order through each query's slot.  Validation happens
+// here, before anything runs (batch.py:112-148).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__ TreeDev T, int kind,
                                                          const i64* __restrict__ ids,
@@ -285,22 +286,41 @@ __global__ void __launch_bounds__(1024) qsort_scan_kernel(u32* __restrict__ hist
   }
 }
 
-// the sorted batch: (argument | id << 48) and the query index -- 12 bytes
-// of scattered writes per query (ids ride in the argument's top bits:
-// positions / ordinals stay below 2^48; the id is the bucket's top bits)
+// the sorted batch: (argument | id << 48) -- 8 bytes of scattered writes per
+// query (ids ride in the argument's top bits: positions / ordinals stay below
+// 2^48; the id is the bucket's top bits) -- and, in query order, the slot each
+// query went to (a coalesced write: the results come back by a gather)
 __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restrict__ bucket_of,
                                                              bool with_id, u32 bits_per_sym,
                                                              const i64* __restrict__ args, u64 m,
                                                              u32* __restrict__ cursor,
                                                              i64* __restrict__ sargs,
-                                                             u32* __restrict__ perm) {
+                                                             u32* __restrict__ slot_of) {
   const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
   if (i >= m) return;
   const u32 b = bucket_of[i];
   const u32 slot = atomicAdd(cursor + b, 1u);
   const u64 a = (u64)args[i] & ((1ull << 48) - 1);
   sargs[slot] = (i64)(with_id ? a | ((u64)(b >> bits_per_sym) << 48) : a);
-  perm[slot] = (u32)i;
+  slot_of[i] = slot;
+}
+
+// results back in query order: out[i] = res[slot_of[i]] -- random 8-byte
+// READS (whole sectors, no write-allocate of partial sectors) and coalesced
+// writes, where writing through the permutation from the query kernel cost
+// as much as the queries' own walk
+template <typename T>
+__global__ void __launch_bounds__(Q_NT) qunsort_kernel(const T* __restrict__ res,
+                                                       const u32* __restrict__ slot_of,
+                                                       T* __restrict__ out, u64 m) {
+  const u64 i0 = ((u64)blockIdx.x * Q_NT + threadIdx.x) * 4;
+  if (i0 + 4 <= m) {
+    const uint4 s = *reinterpret_cast<const uint4*>(slot_of + i0);
+    const T a = __ldg(res + s.x), b = __ldg(res + s.y), c = __ldg(res + s.z), d = __ldg(res + s.w);
+    out[i0] = a; out[i0 + 1] = b; out[i0 + 2] = c; out[i0 + 3] = d;
+  } else {
+    for (u64 i = i0; i < m; ++i) out[i] = res[slot_of[i]];
+  }
 }
 
 cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool validate,
@@ -325,14 +345,25 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
                                                       base, bad);
   qsort_scan_kernel<<<1, 1024, 0, st>>>(S.hist, nb);
   qsort_scatter_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(S.bucket_of, kind != 0, bits_per_sym,
-                                                          args, m, S.hist, S.sorted_args, S.perm);
+                                                          args, m, S.hist, S.sorted_args, S.slot_of);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // ids are mapped minimal ids now (packed into the arguments): run
   // unvalidated -- validation happened above; invalid queries are clamped
-  // into range by the walk and the batch raises anyway
-  return launch_query(T, kind, out_kind, false, nullptr, S.sorted_args, out, m, rate_log, base,
-                      bad, st, S.perm);
+  // into range by the walk and the batch raises anyway.  Results land in
+  // sorted order (coalesced), then one gather puts them in query order.
+  e = launch_query(T, kind, out_kind, false, nullptr, S.sorted_args, S.res, m, rate_log, base, bad,
+                   st, true);
+  if (e != cudaSuccess) return e;
+  const unsigned ub = (unsigned)((m + 4 * Q_NT - 1) / (4 * Q_NT));
+  const int ob = kind == 0 ? out_kind : 8;
+  if (ob == 1)
+    qunsort_kernel<u8><<<ub, Q_NT, 0, st>>>((const u8*)S.res, S.slot_of, (u8*)out, m);
+  else if (ob == 2)
+    qunsort_kernel<u16><<<ub, Q_NT, 0, st>>>((const u16*)S.res, S.slot_of, (u16*)out, m);
+  else
+    qunsort_kernel<u64><<<ub, Q_NT, 0, st>>>((const u64*)S.res, S.slot_of, (u64*)out, m);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------

@@ -894,7 +894,7 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
       const uint64_t slice = std::min<uint64_t>(m, 1ull << 31);
       Scratch S{{}, st};
       QuerySortScratch Q{};
-      TRY(S.get(&Q.hist, 65536));
+      TRY(S.get(&Q.hist, (1u << kQSortMaxBits) + 256));
       TRY(S.get(&Q.bucket_of, slice));
       TRY(S.get(&Q.sorted_args, slice));
       TRY(S.get(&Q.slot_of, slice));
@@ -935,7 +935,8 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
   const bool sorted = (flags & WT_F_SORT) != 0;
   // per slot: ids, args, out [+ sort scratch: buckets, slot_of, sorted args,
   // bucket_of, sorted-order results; each 16-byte aligned]
-  const size_t sort_bytes = sorted ? 65536 * 4 + chunk * (4 + 8 + 4 + out_elem) + 5 * 16 : 0;
+  const size_t sort_bytes =
+      sorted ? ((1u << kQSortMaxBits) + 256) * 4 + chunk * (4 + 8 + 4 + out_elem) + 5 * 16 : 0;
   const size_t need = chunk * (16 + out_elem) + 64 + sort_bytes;
   for (int i = 0; i < 3; ++i) {
     if (!t->qstream[i]) CU(cudaStreamCreateWithFlags(&t->qstream[i], cudaStreamNonBlocking));
@@ -990,7 +991,7 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
         sp = (u8*)(((uintptr_t)(sp + bytes) + 15) & ~(uintptr_t)15);
         return p;
       };
-      Q.hist = (u32*)take(65536 * 4);
+      Q.hist = (u32*)take(((1u << kQSortMaxBits) + 256) * 4);
       Q.slot_of = (u32*)take(chunk * 4);
       Q.sorted_args = (i64*)take(chunk * 8);
       Q.bucket_of = (u32*)take(chunk * 4);

@@ -59,10 +59,11 @@ cudaError_t launch_query(const TreeDev& T, int kind, int out_kind, bool validate
                          const i64* args, void* out, u64 m, int rate_log, u64 base, u64* bad,
                          cudaStream_t st, bool packed = false);
 
-// device sort_queries_by_symbol: counting sort into 65536 buckets, then the
+// device sort_queries_by_symbol: counting sort into <= 2^20 buckets, then the
 // query kernel on the sorted batch writing results back in query order
+constexpr u32 kQSortMaxBits = 20;  // at most 2^20 sort buckets
 struct QuerySortScratch {
-  u32* hist;        // 65536 bucket counts / cursors
+  u32* hist;        // (1 << kQSortMaxBits) bucket counts / cursors + 256 scan partials
   u32* bucket_of;   // m (the minimal id is the bucket's top bits)
   i64* sorted_args; // m: argument | id << 48
   u32* slot_of;     // m: sorted slot of each query (query order)

@@ -196,7 +196,7 @@ cudaError_t launch_query(const TreeDev& T, int kind, int out_kind, bool validate
 
 // ---------------------------------------------------------------------------
 // sort_queries_by_symbol on the device (batch.py:61-75):
-// a counting sort into at most 65,536 buckets -- (symbol id, coarse
+// a counting sort into 2^10 .. 2^20 buckets (about 32 queries each) -- (symbol id, coarse
 // position / ordinal) for rank / select, coarse position for access -- so
 // queries that walk the same nodes and nearby lines run side by side.
 // The query kernel writes results in sorted order; qunsort_kernel gathers
@@ -241,27 +241,52 @@ __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__
   atomicAdd(hist + bucket, 1u);
 }
 
-// one CTA: exclusive scan of the 65536 bucket counts in place (64 per
-// thread, read as uint4 so the loads are independent)
-__global__ void __launch_bounds__(1024) qsort_scan_kernel(u32* __restrict__ hist, u32 nb) {
+// exclusive scan of the bucket counts in place, 4096 buckets per CTA (1024
+// threads x uint4): pass 1 writes each CTA's total, pass 2 adds the totals of
+// the CTAs before it (<= 256 of them) and scans its own buckets
+constexpr int QS_PER_CTA = 4096;
+__device__ __forceinline__ u32 qs_block_sum(u32 v, u32* wsum) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  __syncthreads();
+  if (lane == 0) wsum[warp] = v;
+  __syncthreads();
+  u32 t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0u;
+#pragma unroll
+  for (int d = 16; d; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+  return t;
+}
+__device__ __forceinline__ uint4 qs_load(const u32* hist, u32 nb, u32 i4) {
+  if ((i4 + 1) * 4 <= nb) return reinterpret_cast<const uint4*>(hist)[i4];
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (i4 * 4 + 0 < nb) v.x = hist[i4 * 4 + 0];
+  if (i4 * 4 + 1 < nb) v.y = hist[i4 * 4 + 1];
+  if (i4 * 4 + 2 < nb) v.z = hist[i4 * 4 + 2];
+  return v;
+}
+__global__ void __launch_bounds__(1024) qsort_scan_partial_kernel(const u32* __restrict__ hist, u32 nb,
+                                                                  u32* __restrict__ partial) {
+  __shared__ u32 wsum[32];
+  const uint4 v = qs_load(hist, nb, blockIdx.x * (QS_PER_CTA / 4) + threadIdx.x);
+  const u32 t = qs_block_sum(v.x + v.y + v.z + v.w, wsum);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+__global__ void __launch_bounds__(1024) qsort_scan_final_kernel(u32* __restrict__ hist, u32 nb,
+                                                                const u32* __restrict__ partial) {
   __shared__ u32 wsum[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int PER = 64;  // nb == 65536
-  (void)nb;
-  uint4* h4 = reinterpret_cast<uint4*>(hist) + tid * (PER / 4);
-  uint4 v[PER / 4];
-  u32 sum = 0;
-#pragma unroll
-  for (int k = 0; k < PER / 4; ++k) {
-    v[k] = h4[k];
-    sum += v[k].x + v[k].y + v[k].z + v[k].w;
-  }
+  const u32 off = qs_block_sum(tid < (int)blockIdx.x ? partial[tid] : 0u, wsum);
+  const u32 i4 = blockIdx.x * (QS_PER_CTA / 4) + tid;
+  const uint4 v = qs_load(hist, nb, i4);
+  const u32 sum = v.x + v.y + v.z + v.w;
   u32 inc = sum;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const u32 y = __shfl_up_sync(0xffffffffu, inc, d);
     if (lane >= d) inc += y;
   }
+  __syncthreads();
   if (lane == 31) wsum[warp] = inc;
   __syncthreads();
   if (warp == 0) {
@@ -274,15 +299,12 @@ __global__ void __launch_bounds__(1024) qsort_scan_kernel(u32* __restrict__ hist
     wsum[lane] = t;
   }
   __syncthreads();
-  u32 run = (warp ? wsum[warp - 1] : 0) + inc - sum;
+  u32 run = off + (warp ? wsum[warp - 1] : 0u) + inc - sum;
+  const u32 e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-  for (int k = 0; k < PER / 4; ++k) {
-    uint4 o;
-    o.x = run; run += v[k].x;
-    o.y = run; run += v[k].y;
-    o.z = run; run += v[k].z;
-    o.w = run; run += v[k].w;
-    h4[k] = o;
+  for (int j = 0; j < 4; ++j) {
+    if (i4 * 4 + j < nb) hist[i4 * 4 + j] = run;
+    run += e[j];
   }
 }
 
@@ -329,21 +351,29 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   if (m == 0) return cudaSuccess;
   if (m > 0xffffffffull) return cudaErrorInvalidValue;
   const u64 blocks = (m + Q_NT - 1) / Q_NT;
-  // bucket layout: symbol bits + argument bits <= 16
+  // buckets: about 32 queries each (2^10 .. 2^20 of them) -- a warp's
+  // queries then share nodes and lines at every level; bucket = symbol id
+  // bits + argument bits
+  u32 qb = 10;
+  while (qb < kQSortMaxBits && (1ull << (qb + 5)) < m) ++qb;
   u32 sym_bits = 0;
   if (kind != 0)
     while ((1u << sym_bits) < T.sigma) ++sym_bits;
-  const u32 bits_per_sym = 16 - sym_bits;
+  if (qb < sym_bits) qb = sym_bits;
+  const u32 bits_per_sym = qb - sym_bits;
   const u64 arg_span = kind == 2 ? S.max_occ : T.n + 1;  // args in [0, arg_span)
   u32 arg_shift = 0;  // the largest argument must fit in bits_per_sym bits
   while (((arg_span - 1) >> arg_shift) >= (1ull << bits_per_sym)) ++arg_shift;
-  const u32 nb = 1u << 16;
+  const u32 nb = 1u << qb;
   cudaError_t e = cudaMemsetAsync(S.hist, 0, nb * 4, st);
   if (e != cudaSuccess) return e;
   qsort_key_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(T, kind, ids, args, m, validate, bits_per_sym,
                                                       arg_shift, S.bucket_of, S.hist,
                                                       base, bad);
-  qsort_scan_kernel<<<1, 1024, 0, st>>>(S.hist, nb);
+  const unsigned sb = (nb + QS_PER_CTA - 1) / QS_PER_CTA;
+  u32* partial = S.hist + (1u << kQSortMaxBits);
+  qsort_scan_partial_kernel<<<sb, 1024, 0, st>>>(S.hist, nb, partial);
+  qsort_scan_final_kernel<<<sb, 1024, 0, st>>>(S.hist, nb, partial);
   qsort_scatter_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(S.bucket_of, kind != 0, bits_per_sym,
                                                           args, m, S.hist, S.sorted_args, S.slot_of);
   e = cudaGetLastError();

@@ -183,3 +183,28 @@ def test_level0_block_mode(W, name, monkeypatch):
     t = W.construct(text)
     assert_same_structure(t, O.build(text))
     _check_queries(W, t, text, t.alphabet.sorted_symbols, m=5000)
+
+
+def test_device_query_sort_unaligned_inputs(W):
+    """Device-resident batches starting at an odd element (8-byte, not 16-byte
+    aligned) and odd lengths through the sorted path."""
+    import ctypes as C
+    import torch
+    from paper_2505_03372_b200 import _lib
+    text = np.random.default_rng(51).integers(0, 256, 1 << 20, dtype=np.uint8)
+    t = W.construct(text)
+    r = np.random.default_rng(52)
+    m = 10001
+    ids = t.alphabet.sorted_symbols[r.integers(0, t.sigma, m + 1)].astype(np.int64)
+    pos = r.integers(0, len(text) + 1, m + 1)
+    d_ids = torch.from_numpy(ids).cuda()[1:]
+    d_pos = torch.from_numpy(pos).cuda()[1:]
+    assert d_pos.data_ptr() % 16 == 8
+    out = torch.empty(m, dtype=torch.int64, device="cuda")
+    bad = C.c_int64(-1)
+    _lib.check(_lib.lib.wt_tree_query(t.handle, _lib.Q_RANK, C.c_void_p(d_ids.data_ptr()),
+                                      C.c_void_p(d_pos.data_ptr()), C.c_void_p(out.data_ptr()), m, 0,
+                                      _lib.F_DEVICE_PTRS | _lib.F_SYMBOLS | _lib.F_SORT, None,
+                                      C.byref(bad), None))
+    assert bad.value == -1
+    assert np.array_equal(out.cpu().numpy(), W.rank_batch(t, ids[1:], pos[1:]))

@@ -303,7 +303,7 @@ def run_ours(args):
     if args.e2e:
         pin = lambda t: t.cpu().pin_memory().numpy()
         h_acc, h_rsym, h_rpos, h_ssym, h_ks = map(pin, (q_acc, q_rsym, q_rpos, q_ssym, q_ks))
-        chunk = 1 << 22  # 8 chunks per kind: the copy-in / kernel / copy-out pipeline overlaps
+        chunk = 1 << 21  # 16 chunks per kind: the copy-in / kernel / copy-out pipeline overlaps
         for _ in range(max(2, args.warmup)):  # also fills the pinned result-array cache
             ra = W.access_batch(tree, h_acc, chunk_size=chunk, sort="access" in sort_kinds)
             rr = W.rank_batch(tree, h_rsym, h_rpos, chunk_size=chunk, sort="rank" in sort_kinds)
@@ -347,7 +347,7 @@ def run_ours(args):
                              % (tree.device_bytes / 1e9, m_total * 16 / 1e9)},
             "queries": queries, "build": build, "replicate": replicate,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps * sum(4 if b[0] in sort_kinds else 1 for b in batches),
+            "gpu_launches": args.steps * sum(6 if b[0] in sort_kinds else 1 for b in batches),
             "clocks": clk.summary(),
         }
         print(json.dumps(line))

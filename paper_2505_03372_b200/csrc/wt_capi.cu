@@ -858,13 +858,6 @@ extern "C" int wt_tree_destroy(wt_tree* t) {
 // ---------------------------------------------------------------------------
 // queries
 // ---------------------------------------------------------------------------
-static u64 max_occ(const wt_tree* t) {
-  u64 mx = 1;
-  for (uint32_t i = 0; i < t->plan.sigma; ++i)
-    mx = std::max<u64>(mx, (u64)(t->plan.cum[i + 1] - t->plan.cum[i]));
-  return mx;
-}
-
 extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int64_t* args,
                              void* out, uint64_t m, uint64_t chunk, int flags, void* stream,
                              int64_t* bad_index, float* ms_out) {
@@ -903,7 +896,6 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
         TRY(S.get(&r, slice * out_elem));
         Q.res = r;
       }
-      Q.max_occ = max_occ(t);
       for (uint64_t a = 0; a < m; a += slice) {
         const uint64_t cnt = std::min(slice, m - a);
         CU(launch_query_sorted(t->dev, kind, out_kind, validate,
@@ -996,7 +988,6 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
       Q.sorted_args = (i64*)take(chunk * 8);
       Q.bucket_of = (u32*)take(chunk * 4);
       Q.res = take(chunk * out_elem);
-      Q.max_occ = max_occ(t);
       e = launch_query_sorted(t->dev, kind, out_kind, validate, d_ids, d_args, d_out, cnt,
                               t->rate_log, a, t->bad, Q, sk);
     }

@@ -206,7 +206,7 @@ cudaError_t launch_query(const TreeDev& T, int kind, int out_kind, bool validate
 __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__ TreeDev T, int kind,
                                                          const i64* __restrict__ ids,
                                                          const i64* __restrict__ args, u64 m,
-                                                         bool validate, u32 bits_per_sym,
+                                                         bool validate, u32 sym_bits,
                                                          u32 arg_shift, u32* __restrict__ bucket_of,
                                                          u32* __restrict__ hist, u64 base,
                                                          u64* __restrict__ bad) {
@@ -232,9 +232,21 @@ __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__
       if (kind == 1) ok = a <= T.n;
       else ok = a >= 1 && (i64)a <= __ldg(T.cum + c + 1) - __ldg(T.cum + c);
     }
-    const u64 sub = kind == 1 ? a : a - 1;
-    // (the bucket's top bits are the minimal id: the scatter recovers it)
-    bucket = ok ? (c << bits_per_sym) | (u32)(sub >> arg_shift) : 0u;
+    // Position-block major, symbol minor: consecutive buckets walk the same
+    // stretch of the text -- and so of every level's nodes -- for all
+    // symbols, which keeps each level's lines in L2 while the stretch runs
+    // (symbol-major buckets re-read the upper levels once per symbol).
+    // select orders by the estimated text position k * n / occ(c).  The low
+    // bits are the minimal id: the scatter recovers it.
+    if (ok) {
+      u64 est = a;
+      if (kind == 2) {
+        const i64 occ = __ldg(T.cum + c + 1) - __ldg(T.cum + c);
+        const float f = (float)(a - 1) * ((float)T.n / (float)(occ > 0 ? occ : 1));
+        est = min((u64)f, T.n);
+      }
+      bucket = ((u32)(est >> arg_shift) << sym_bits) | c;
+    }
   }
   if (!ok) atomicMin(bad, base + i);
   bucket_of[i] = bucket;
@@ -313,7 +325,7 @@ __global__ void __launch_bounds__(1024) qsort_scan_final_kernel(u32* __restrict_
 // 2^48; the id is the bucket's top bits) -- and, in query order, the slot each
 // query went to (a coalesced write: the results come back by a gather)
 __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restrict__ bucket_of,
-                                                             bool with_id, u32 bits_per_sym,
+                                                             bool with_id, u32 sym_bits,
                                                              const i64* __restrict__ args, u64 m,
                                                              u32* __restrict__ cursor,
                                                              i64* __restrict__ sargs,
@@ -323,7 +335,7 @@ __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restri
   const u32 b = bucket_of[i];
   const u32 slot = atomicAdd(cursor + b, 1u);
   const u64 a = (u64)args[i] & ((1ull << 48) - 1);
-  sargs[slot] = (i64)(with_id ? a | ((u64)(b >> bits_per_sym) << 48) : a);
+  sargs[slot] = (i64)(with_id ? a | ((u64)(b & ((1u << sym_bits) - 1u)) << 48) : a);
   slot_of[i] = slot;
 }
 
@@ -360,21 +372,20 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   if (kind != 0)
     while ((1u << sym_bits) < T.sigma) ++sym_bits;
   if (qb < sym_bits) qb = sym_bits;
-  const u32 bits_per_sym = qb - sym_bits;
-  const u64 arg_span = kind == 2 ? S.max_occ : T.n + 1;  // args in [0, arg_span)
-  u32 arg_shift = 0;  // the largest argument must fit in bits_per_sym bits
-  while (((arg_span - 1) >> arg_shift) >= (1ull << bits_per_sym)) ++arg_shift;
+  const u32 pos_bits = qb - sym_bits;
+  u32 arg_shift = 0;  // positions [0, n] must fit in pos_bits bits
+  while ((T.n >> arg_shift) >= (1ull << pos_bits)) ++arg_shift;
   const u32 nb = 1u << qb;
   cudaError_t e = cudaMemsetAsync(S.hist, 0, nb * 4, st);
   if (e != cudaSuccess) return e;
-  qsort_key_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(T, kind, ids, args, m, validate, bits_per_sym,
+  qsort_key_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(T, kind, ids, args, m, validate, sym_bits,
                                                       arg_shift, S.bucket_of, S.hist,
                                                       base, bad);
   const unsigned sb = (nb + QS_PER_CTA - 1) / QS_PER_CTA;
   u32* partial = S.hist + (1u << kQSortMaxBits);
   qsort_scan_partial_kernel<<<sb, 1024, 0, st>>>(S.hist, nb, partial);
   qsort_scan_final_kernel<<<sb, 1024, 0, st>>>(S.hist, nb, partial);
-  qsort_scatter_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(S.bucket_of, kind != 0, bits_per_sym,
+  qsort_scatter_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(S.bucket_of, kind != 0, sym_bits,
                                                           args, m, S.hist, S.sorted_args, S.slot_of);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;

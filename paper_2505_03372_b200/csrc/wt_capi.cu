@@ -316,7 +316,7 @@ static int alloc_tree(wt_tree* t, cudaStream_t st) {
     TRY(dalloc(&h.zeros, m / t->meta.sample_rate, st));
     h.n_lines = qlayout_lines(m);
     h.sel_cap = (m >> kQSelLog) + 2;
-    TRY(dalloc(&h.lines, h.n_lines * 4, st));
+    TRY(dalloc(&h.lines, h.n_lines * kQLineU2, st));
     TRY(dalloc(&h.sel1, h.sel_cap, st));
     TRY(dalloc(&h.sel0, h.sel_cap, st));
   }
@@ -342,7 +342,7 @@ static int alloc_tree(wt_tree* t, cudaStream_t st) {
   uint64_t bytes = P.n_words * 8 + P.nodes.size() * sizeof(NodeEnt) + P.sigma * 14 + 8;
   for (auto& h : t->lv)
     bytes += h.meta.n_l1 * 8 + h.meta.n_l2 * 2 + 2 * (h.meta.n_bits / t->meta.sample_rate) * 8 +
-             h.n_lines * 64 + 2 * h.sel_cap * 4;
+             h.n_lines * kQLineBytes + 2 * h.sel_cap * 4;
   t->meta.device_bytes = bytes;
   return WT_OK;
 }
@@ -562,7 +562,7 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       uint64_t est = P.n_words * 8 + 64ull * 1024 * 1024;
       for (uint32_t l = 0; l < P.L; ++l) {
         const uint64_t m = (uint64_t)P.sizes[l];
-        est += m / 7 + m / 32 + m / 256 + 2 * (m / sample_rate) * 8 + (m >> kQSelLog) * 8;
+        est += m * kQLineBytes / kQBits + m / 32 + m / 256 + 2 * (m / sample_rate) * 8 + (m >> kQSelLog) * 8;
         if (l == 1 || l == 2) est += m * P.code_bytes;
       }
       void* probe = nullptr;

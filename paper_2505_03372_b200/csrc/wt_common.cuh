@@ -49,15 +49,26 @@ struct LevelDev {
   u64 n_bits, total_ones, n_ones, n_zeros, n_l1, n_l2;
 };
 
-// Query-side layout of one level ("rank lines"): 64-byte lines, word 0 =
-// ones before the line (absolute), words 1..7 = 448 bits of the level.  A
-// rank step touches exactly one line; select narrows to a few lines through
-// a line index per kQSel-th one / zero.  Built from the reference layout by
+// Query-side layout of one level ("rank lines"): 32-byte lines (one sector,
+// one LDG.256), word 0 = ones before the line (absolute), words 1..kQW = the
+// next 64*kQW bits of the level.  A rank step touches exactly one line;
+// select narrows to a few lines through a line index per 2^kQSelLog-th one /
+// zero.  (64-byte lines of 448 bits, WT_QW=7, halve the header overhead but
+// double the sectors and L1 wavefronts per step.)  Built from the reference layout by
 // qlayout_kernel; exports keep the reference layout (wtree.py / bitvec.py).
-constexpr int kQBits = 448;
-constexpr int kQSelLog = 7;  // one select sample per 128 ones / zeros
+#ifndef WT_QW
+#define WT_QW 3
+#endif
+constexpr int kQW = WT_QW;                // data words per line (3: 32-byte lines, 7: 64-byte)
+constexpr int kQBits = 64 * kQW;          // bits per line
+constexpr int kQLineBytes = 8 * (kQW + 1);
+constexpr int kQLineU2 = kQLineBytes / 16;  // ulonglong2 per line
+#ifndef WT_QSEL_LOG
+#define WT_QSEL_LOG 6
+#endif
+constexpr int kQSelLog = WT_QSEL_LOG;  // one select sample per 2^kQSelLog ones / zeros
 struct QLevelDev {
-  const ulonglong2* lines;  // 4 x 16 B per line
+  const ulonglong2* lines;  // kQLineU2 x 16 B per line
   const u32* sel1;          // line holding the (j*128+1)-th one
   const u32* sel0;
   u64 n_lines, n_sel1, n_sel0, n_bits, total_ones;

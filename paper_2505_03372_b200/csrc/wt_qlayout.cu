@@ -1,11 +1,12 @@
 // wt_qlayout.cu -- query-side "rank line" layout of each level.
 //
-// Line i of a level = [ones before bit 448 i | bits 448 i .. 448 i + 447].
-// One thread per line: the 7 data words are a straight copy (448 = 7 x 64,
-// word aligned), the header comes from the level's reference directory
+// Line i of a level = [ones before bit kQBits i | the next kQBits bits].
+// One thread per line: the kQW data words are a straight copy (word
+// aligned), the header comes from the level's reference directory
 // (rank1 = L1 + L2 + popcount, rankselect.py:151-169) and the thread emits
-// the select samples (line index of every 128-th one / zero) that fall in
-// its line (every 128-th).  The last line is a sentinel whose header is the level total.
+// the select samples (line index of every 2^kQSelLog-th one / zero) that
+// fall in its line.  The last line is a sentinel whose header is the level
+// total.
 #include "wt_common.cuh"
 #include "wt_kernels.h"
 #include "wt_rs.cuh"
@@ -23,21 +24,20 @@ __global__ void __launch_bounds__(QL_NT) qlayout_kernel(LevelDev L, const u64* t
   L.total_ones = *total;
   const u64 b0 = i * kQBits;
   const u64 nw = (L.n_bits + 63) >> 6;
-  u64 w[7];
+  u64 w[kQW];
   u32 pc = 0;
 #pragma unroll
-  for (int x = 0; x < 7; ++x) {
+  for (int x = 0; x < kQW; ++x) {
     const u64 wi = (b0 >> 6) + x;
     w[x] = wi < nw ? __ldg(L.words + wi) : 0ull;  // padding bits are zero
     pc += __popcll(w[x]);
   }
   const u64 hdr = b0 >= L.n_bits ? L.total_ones : rank1_dev(L, b0, l2_shift);
-  ulonglong2* out = lines + i * 4;
+  ulonglong2* out = lines + i * kQLineU2;
   out[0] = make_ulonglong2(hdr, w[0]);
-  out[1] = make_ulonglong2(w[1], w[2]);
-  out[2] = make_ulonglong2(w[3], w[4]);
-  out[3] = make_ulonglong2(w[5], w[6]);
-  // samples: ordinals k = j*128 + 1 in (hdr, hdr + pc] for ones, likewise zeros
+#pragma unroll
+  for (int x = 1; x < kQLineU2; ++x) out[x] = make_ulonglong2(w[2 * x - 1], w[2 * x]);
+  // samples: ordinals k = j * 2^kQSelLog + 1 in (hdr, hdr + pc] for ones, likewise zeros
   if (pc) {
     const u64 lo = hdr, hi = hdr + pc;
     for (u64 j = (lo + (1u << kQSelLog) - 1) >> kQSelLog; (j << kQSelLog) + 1 <= hi; ++j)

@@ -90,15 +90,21 @@ namespace wt {
 // rank / select on the query-side rank-line layout (wt_qlayout.cu)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ u64 qline_of(u64 p, u32& w) {
-  const u64 q = p >> 6;                                    // word index in the level
-  const u64 i = __umul64hi(q, 0x2492492492492493ull);      // q / 7 (exact for q < 2^61)
-  w = (u32)(q - 7 * i);
+  const u64 q = p >> 6;  // word index in the level
+  u64 i;
+  if (kQW == 7)
+    i = __umul64hi(q, 0x2492492492492493ull);     // q / 7 (exact for q < 2^61)
+  else if (kQW == 3)
+    i = __umul64hi(q, 0xAAAAAAAAAAAAAAABull) >> 1;  // q / 3
+  else
+    i = q / kQW;
+  w = (u32)(q - kQW * i);
   return i;
 }
 
 struct QLine {
   u64 hdr;
-  u64 wd[7];
+  u64 wd[kQW];
 };
 
 // Random 64-byte line reads: hint the L2 to fetch 64 B (LTC64B) instead of
@@ -127,11 +133,21 @@ __device__ __forceinline__ void ld_line32(const ulonglong2* p, u64& a, u64& b, u
                : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
                : "l"(p));
 }
+static_assert(kQW == 3 || kQW == 7, "line width: one 32-byte sector or 64 bytes");
+__device__ __forceinline__ void ld_sector(const ulonglong2* p, u64& a, u64& b, u64& c, u64& d) {
+  asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+               : "l"(p));
+}
 __device__ __forceinline__ QLine qload(const QLevelDev& Q, u64 i) {
-  const ulonglong2* L = Q.lines + i * 4;
+  const ulonglong2* L = Q.lines + i * kQLineU2;
   QLine r;
-  ld_line32(L, r.hdr, r.wd[0], r.wd[1], r.wd[2]);
-  ld_line32(L + 2, r.wd[3], r.wd[4], r.wd[5], r.wd[6]);
+  if constexpr (kQW == 3) {
+    ld_sector(L, r.hdr, r.wd[0], r.wd[1], r.wd[2]);
+  } else {
+    ld_line32(L, r.hdr, r.wd[0], r.wd[1], r.wd[2]);
+    ld_line32(L + 2, r.wd[kQW - 4], r.wd[kQW - 3], r.wd[kQW - 2], r.wd[kQW - 1]);
+  }
   return r;
 }
 
@@ -140,7 +156,7 @@ __device__ __forceinline__ u64 qline_prefix(const QLine& L, u32 w, u64& word) {
   u64 r = L.hdr;
   word = L.wd[0];
 #pragma unroll
-  for (int x = 0; x < 7; ++x) {
+  for (int x = 0; x < kQW; ++x) {
     if ((u32)x < w) r += __popcll(L.wd[x]);
     if ((u32)x == w) word = L.wd[x];
   }
@@ -179,7 +195,7 @@ __device__ __forceinline__ u64 qselect(const QLevelDev& Q, u64 k) {
   u64 hi = j + 1 < ns ? (u64)ld_u32_64b(sel + j + 1) : Q.n_lines - 1;
   while (lo < hi) {  // last line whose count before it is below k
     const u64 mid = (lo + hi + 1) >> 1;
-    const u64 h = ld_u64_64b(reinterpret_cast<const u64*>(Q.lines + mid * 4));
+    const u64 h = ld_u64_64b(reinterpret_cast<const u64*>(Q.lines + mid * kQLineU2));
     const u64 v = kOnes ? h : mid * kQBits - h;
     if (v < k) lo = mid; else hi = mid - 1;
   }
@@ -187,11 +203,11 @@ __device__ __forceinline__ u64 qselect(const QLevelDev& Q, u64 k) {
   k -= kOnes ? L.hdr : lo * kQBits - L.hdr;
   // find the word first (predicated selects), then ONE in-word select: inside
   // the loop it would run once per distinct word index in the warp
-  u32 wi = 6, kk = (u32)k;
-  u64 ws = kOnes ? L.wd[6] : ~L.wd[6];
+  u32 wi = kQW - 1, kk = (u32)k;
+  u64 ws = kOnes ? L.wd[kQW - 1] : ~L.wd[kQW - 1];
   bool done = false;
 #pragma unroll
-  for (int x = 0; x < 6; ++x) {
+  for (int x = 0; x < kQW - 1; ++x) {
     const u64 word = kOnes ? L.wd[x] : ~L.wd[x];
     const u32 pc = __popcll(word);
     const bool here = !done && pc >= kk;

@@ -28,18 +28,20 @@ def main():
     ssym = pin(syms[sid])
     ks = pin(torch.minimum(1 + (torch.rand(m, generator=g, device="cuda", dtype=torch.float64)
                                 * occ[sid]).long(), occ[sid]))
-    for log in (20, 21, 22, 23):
+    for log in (16, 18, 20, 21, 22):
         c = 1 << log
-        ts = []
-        for r in range(5):
-            t0 = time.perf_counter()
-            W.access_batch(tree, acc, chunk_size=c, sort=True)
-            W.rank_batch(tree, rsym, rpos, chunk_size=c, sort=True)
-            W.select_batch(tree, ssym, ks, chunk_size=c, sort=True)
-            if r >= 2:
-                ts.append(time.perf_counter() - t0)
-        t = float(np.median(ts))
-        print(f"chunk 2^{log}: {3 * m / t / 1e9:.3f} G q/s  ({t * 1e3:.1f} ms per 3 batches)", flush=True)
+        for srt in (False, True):
+            ts = []
+            for r in range(4):
+                t0 = time.perf_counter()
+                W.access_batch(tree, acc, chunk_size=c, sort=srt)
+                W.rank_batch(tree, rsym, rpos, chunk_size=c, sort=srt)
+                W.select_batch(tree, ssym, ks, chunk_size=c, sort=srt)
+                if r >= 1:
+                    ts.append(time.perf_counter() - t0)
+            t = float(np.median(ts))
+            print(f"chunk 2^{log} sort={srt}: {3 * m / t / 1e9:.3f} G q/s  ({t * 1e3:.1f} ms per 3 batches)",
+                  flush=True)
 
 
 if __name__ == "__main__":

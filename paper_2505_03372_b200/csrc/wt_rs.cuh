@@ -126,6 +126,24 @@ __device__ __forceinline__ u32 ld_u32_64b(const u32* p) {
   return v;
 }
 
+// batch streams (arguments in, results out): L2 evict-first, so the walk's
+// lines keep the L2
+__device__ __forceinline__ u64 l2_evict_first_policy() {
+  u64 p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ i64 ld_stream_i64(const i64* a, u64 pol) {
+  i64 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
+               : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_stream_i64(i64* a, i64 v, u64 pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(a), "l"(v), "l"(pol)
+               : "memory");
+}
+
 // one 64-byte line as two 256-bit loads (LDG.256, sm_100): half the LSU
 // instructions of 16-byte loads, which kept the query kernels lg-throttled
 __device__ __forceinline__ void ld_line32(const ulonglong2* p, u64& a, u64& b, u64& c, u64& d) {

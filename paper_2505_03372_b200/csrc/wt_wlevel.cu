@@ -465,19 +465,6 @@ __device__ __forceinline__ void st_shared(u32 addr, u32 v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v));
 }
 
-// SWAR count of bit `sh` of every code in a 16-byte chunk
-template <typename TC>
-__device__ __forceinline__ u32 wswar16(uint4 v, u32 sh) {
-  if (sizeof(TC) == 1) {
-    const u32 y = ((v.x >> sh) & 0x01010101u) + ((v.y >> sh) & 0x01010101u) +
-                  ((v.z >> sh) & 0x01010101u) + ((v.w >> sh) & 0x01010101u);
-    return (y * 0x01010101u) >> 24;
-  }
-  const u32 y = ((v.x >> sh) & 0x00010001u) + ((v.y >> sh) & 0x00010001u) +
-                ((v.z >> sh) & 0x00010001u) + ((v.w >> sh) & 0x00010001u);
-  return (y * 0x00010001u) >> 16;
-}
-
 // one element of a staged run, next-level bit
 template <typename TC>
 __device__ __forceinline__ u32 wbit_at(const u8* stage, u32 byte, u32 sh) {
@@ -487,36 +474,51 @@ __device__ __forceinline__ u32 wbit_at(const u8* stage, u32 byte, u32 sh) {
 
 // next-level ones of the zeros run (Z elements at stage byte zoff, global
 // destination zdst) and of the ones run (O at ooff, odst), per next-level tile
-// (a run spans <= 3) and L1 block.  One pass over the aligned 16-byte chunks
-// of both runs (SWAR), element-wise passes for the run heads / tails and for
-// the parts of the chunks holding a tile boundary; prefix counts up to the
-// boundaries give the split.  Lanes 0..5 add the six counts.
+// (a run spans <= 2 of them, <= 3 when kThree: u8 text -> u16 codes, whose
+// next tiles are half as long) and L1 block.  Per run, one pass over its
+// aligned 16-byte chunks (AND + POPC per word, no multiply), chunks wholly
+// before a boundary also added to that boundary's prefix; element-wise passes
+// for the run heads / tails and for the chunk holding a boundary.  Lanes 0..5
+// add the counts.
 template <typename TC>
+__device__ __forceinline__ u32 wpop16(uint4 v, u32 msk) {
+  return (u32)(__popc(v.x & msk) + __popc(v.y & msk)) + (u32)(__popc(v.z & msk) + __popc(v.w & msk));
+}
+template <typename TC, bool kThree>
 __device__ __forceinline__ void wcount_tile(const u8* stage, u32 Z, u32 zoff, u64 zdst, u32 O,
                                             u32 ooff, u64 odst, u32 sh, int tile_log,
                                             u32* tcounts, u32* l1counts, int lane) {
   constexpr u32 SZ = sizeof(TC);
   constexpr u32 EPC = 16 / SZ;
   const u64 nt = 1ull << tile_log;
+  const u32 msk = (sizeof(TC) == 1 ? 0x01010101u : 0x00010001u) << sh;
   // per run: head elements h, full chunks nf, tail start ts, boundaries b1 <= b2
   const u32 hz = min(Z, ((16u - (zoff & 15u)) & 15u) / SZ), nfz = (Z - hz) / EPC, tsz = hz + nfz * EPC;
   const u32 ho = min(O, ((16u - (ooff & 15u)) & 15u) / SZ), nfo = (O - ho) / EPC, tso = ho + nfo * EPC;
-  const u32 b1z = min(Z, (u32)((((zdst >> tile_log) + 1) << tile_log) - zdst)), b2z = min(Z, b1z + (u32)nt);
-  const u32 b1o = min(O, (u32)((((odst >> tile_log) + 1) << tile_log) - odst)), b2o = min(O, b1o + (u32)nt);
+  const u32 b1z = min(Z, (u32)((((zdst >> tile_log) + 1) << tile_log) - zdst));
+  const u32 b1o = min(O, (u32)((((odst >> tile_log) + 1) << tile_log) - odst));
+  const u32 b2z = kThree ? min(Z, b1z + (u32)nt) : Z, b2o = kThree ? min(O, b1o + (u32)nt) : O;
   u32 az = 0, p1z = 0, p2z = 0, ao = 0, p1o = 0, p2o = 0;
-  for (u32 c = lane; c < nfz + nfo; c += 32) {
-    const bool one = c >= nfz;
-    const u32 i0 = one ? ho + (c - nfz) * EPC : hz + c * EPC;
-    const u32 x = wswar16<TC>(*reinterpret_cast<const uint4*>(stage + (one ? ooff : zoff) + i0 * SZ), sh);
-    const u32 e = i0 + EPC;
-    if (one) {
-      ao += x;
-      p1o += e <= b1o ? x : 0u;
-      p2o += e <= b2o ? x : 0u;
-    } else {
+  {
+    const uint4* cz = reinterpret_cast<const uint4*>(stage + zoff + hz * SZ);
+    const u32 c1 = b1z > hz ? (b1z - hz) / EPC : 0u, c2 = b2z > hz ? (b2z - hz) / EPC : 0u;
+#pragma unroll 2
+    for (u32 c = lane; c < nfz; c += 32) {
+      const u32 x = wpop16<TC>(cz[c], msk);
       az += x;
-      p1z += e <= b1z ? x : 0u;
-      p2z += e <= b2z ? x : 0u;
+      p1z += c < c1 ? x : 0u;
+      if (kThree) p2z += c < c2 ? x : 0u;
+    }
+  }
+  {
+    const uint4* co = reinterpret_cast<const uint4*>(stage + ooff + ho * SZ);
+    const u32 c1 = b1o > ho ? (b1o - ho) / EPC : 0u, c2 = b2o > ho ? (b2o - ho) / EPC : 0u;
+#pragma unroll 2
+    for (u32 c = lane; c < nfo; c += 32) {
+      const u32 x = wpop16<TC>(co[c], msk);
+      ao += x;
+      p1o += c < c1 ? x : 0u;
+      if (kThree) p2o += c < c2 ? x : 0u;
     }
   }
   // element-wise 1: heads and tails (lanes 0-7 z head, 8-15 z tail, 16-23 o head, 24-31 o tail;
@@ -531,9 +533,11 @@ __device__ __forceinline__ void wcount_tile(const u8* stage, u32 Z, u32 zoff, u6
     const u32 bt = in ? wbit_at<TC>(stage, (one ? ooff : zoff) + i * SZ, sh) : 0u;
     const u32 b1 = one ? b1o : b1z, b2 = one ? b2o : b2z;
     if (one) {
-      ao += bt; p1o += i < b1 ? bt : 0u; p2o += i < b2 ? bt : 0u;
+      ao += bt; p1o += i < b1 ? bt : 0u;
+      if (kThree) p2o += i < b2 ? bt : 0u;
     } else {
-      az += bt; p1z += i < b1 ? bt : 0u; p2z += i < b2 ? bt : 0u;
+      az += bt; p1z += i < b1 ? bt : 0u;
+      if (kThree) p2z += i < b2 ? bt : 0u;
     }
   }
   // element-wise 2: the part before each boundary of the full chunk holding it
@@ -542,6 +546,7 @@ __device__ __forceinline__ void wcount_tile(const u8* stage, u32 Z, u32 zoff, u6
   for (int rnd = 0; rnd < 2; ++rnd) {
     const u32 k = (lane & 7) + 8 * rnd;
     const bool one = lane >= 16, second = (lane & 8) != 0;
+    if (!kThree && second) continue;
     const u32 h = one ? ho : hz, ts = one ? tso : tsz;
     const u32 bb = one ? (second ? b2o : b1o) : (second ? b2z : b1z);
     const bool strad = bb > h && bb < ts && ((bb - h) % EPC) != 0;
@@ -559,8 +564,9 @@ __device__ __forceinline__ void wcount_tile(const u8* stage, u32 Z, u32 zoff, u6
   for (int d = 16; d; d >>= 1) {
     q0 += __shfl_xor_sync(FULLM, q0, d);
     q1 += __shfl_xor_sync(FULLM, q1, d);
-    q2 += __shfl_xor_sync(FULLM, q2, d);
+    if (kThree) q2 += __shfl_xor_sync(FULLM, q2, d);
   }
+  if (!kThree) q2 = q0;  // a run spans at most two next-level tiles: nothing past b2
   if (lane < 6) {
     const bool one = lane >= 3;
     const int seg = lane - (one ? 3 : 0);
@@ -973,10 +979,10 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
       }
       // next level's ones of both runs per next-level tile (<= 3 per run) and
       // L1 block, in one pass over the staged tile
-      wcount_tile<TC>(stage, zlive ? zerosA : 0u, zoff, zdst, olive ? onesA : 0u, ooff, odst,
+      wcount_tile<TC, (WS<TIn>::TILE > WS<TC>::TILE)>(stage, zlive ? zerosA : 0u, zoff, zdst, olive ? onesA : 0u, ooff, odst,
                       P.shift_bit - 1, NTILE_LOG, P.next_tile_counts, P.next_l1_counts, lane);
       if (kTwoSeg && split < (u32)TILE)
-        wcount_tile<TC>(stage, zliveB ? zerosB : 0u, zoffB, zdstB, oliveB ? onesB : 0u, ooffB, odstB,
+        wcount_tile<TC, (WS<TIn>::TILE > WS<TC>::TILE)>(stage, zliveB ? zerosB : 0u, zoffB, zdstB, oliveB ? onesB : 0u, ooffB, odstB,
                         P.shift_bit - 1, NTILE_LOG, P.next_tile_counts, P.next_l1_counts, lane);
       if (lane == 0) w_bulk_commit();  // one bulk group per scattering fast tile
     } else {

@@ -6,23 +6,27 @@
 //   build_index (rankselect.py:442-536): L2 entries and select samples
 //   (L1 entries come from the per-L1-block scan that precedes the launch)
 //
-// Every warp owns whole 2 KB tiles (2048 u8 / 1024 u16 elements) and never
-// waits for another warp: no __syncthreads anywhere.  Per tile:
-//   0. the NEXT tile's 2 KB are already in flight into registers (4 x 16 B
-//      per lane, streaming loads issued one tile ahead);
-//   1. SWAR bit extraction -> one mask per 16-byte chunk, packed warp scans of
-//      the ones; the mask is the tile's bit-vector words (u16 / u8 stores);
+// Every warp owns whole tiles of 4 KiB of input (4096 u8 / 2048 u16
+// elements) and never waits for another warp: no __syncthreads in the loop.
+// Per tile:
+//   0. the tile streams into a per-warp shared-memory ring (cp.async.bulk +
+//      mbarrier) two tiles ahead;
+//   1. lane rows: a tile is 16 (u8) / 8 (u16) rows of 256 elements, lane i
+//      owns elements [8i, 8i + 8) of each row; one 8-bit mask per lane-row
+//      (SWAR bit extraction, or `symbol >= thr` at a LUT level 0), packed warp
+//      scans of the row counts; the masks are the tile's bit-vector bytes;
 //   2. P1 (ones before the tile) = L1 prefix of its 65536-bit block + the
-//      counts of the block's earlier tiles (counted by the previous level);
-//   3. single-node tile (the common case): every element goes to a
-//      warp-private staging buffer at its place in the zeros run or the ones
-//      run (offsets congruent to the global destination mod 16); lanes 16..31
-//      walk their chunk from the middle so the two lanes sharing a bank never
-//      store in the same step; each run body leaves as ONE cp.async.bulk
-//      shared -> global store, heads / tails by lanes;
-//   4. the staged runs are scanned (SWAR) for the ones of the NEXT level's
-//      bit per next-level tile / L1 block (a few atomics per run): this is
-//      what makes step 2 possible for the next level without a look-back;
+//      counts of the block's earlier tiles (counted by the previous level;
+//      level 0 of a large u8 text: the warp walks whole blocks, "block mode");
+//   3. single-node tile (the common case; two-node tiles at u16 codes): every
+//      element goes to a warp-private staging buffer at its place in the
+//      zeros run or the ones run (offsets congruent to the global destination
+//      mod 16); each run body leaves as ONE cp.async.bulk shared -> global
+//      store, heads / tails by lanes;
+//   4. the staged runs are counted (AND + POPC) for the ones of the NEXT
+//      level's bit per next-level tile / L1 block (a few atomics per run):
+//      this is what makes step 2 possible for the next level without a
+//      look-back;
 //   5. L2 entries and select samples from (P1, in-tile prefix).
 // Multi-node tiles (node boundaries inside the tile) store element by element.
 // Destination of element j with bit b in node `key`:

@@ -9,6 +9,8 @@
 //           stop when child `bit` of the node is a leaf (width-1 interval);
 //   rank:   the same walk along the code of c, result p_len - cum_hist[c];
 //   select: bottom-up, p = select_bit(p' - base + 1), from cum_hist[c]+k-1.
+#include <cstdio>
+#include <cstdlib>
 #include "wt_common.cuh"
 #include "wt_kernels.h"
 #include "wt_rs.cuh"
@@ -198,8 +200,9 @@ cudaError_t launch_query(const TreeDev& T, int kind, int out_kind, bool validate
 
 // ---------------------------------------------------------------------------
 // sort_queries_by_symbol on the device (batch.py:61-75):
-// a counting sort into 2^10 .. 2^20 buckets (about 32 queries each) -- (symbol id, coarse
-// position / ordinal) for rank / select, coarse position for access -- so
+// a counting sort into 2^10 .. 2^20 buckets (about 128 queries each) --
+// (coarse text position, symbol id) for rank, (coarse estimated position
+// k * n / occ, symbol id) for select, coarse position for access -- so
 // queries that walk the same nodes and nearby lines run side by side.
 // The query kernel writes results in sorted order; qunsort_kernel gathers
 // them back into query order through each query's slot.  Validation happens
@@ -380,11 +383,20 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   if (m == 0) return cudaSuccess;
   if (m > 0xffffffffull) return cudaErrorInvalidValue;
   const u64 blocks = (m + Q_NT - 1) / Q_NT;
-  // buckets: about 32 queries each (2^10 .. 2^20 of them) -- a warp's
-  // queries then share nodes and lines at every level; bucket = symbol id
-  // bits + argument bits
+  // buckets: about 128 queries each (2^10 .. 2^20 of them) -- a warp's
+  // queries then share nodes and lines at every level; bucket = argument
+  // bits over symbol id bits
   u32 qb = 10;
-  while (qb < kQSortMaxBits && (1ull << (qb + 5)) < m) ++qb;
+  u32 qmax = kQSortMaxBits, qlog = 7;  // <= 2^20 buckets of ~2^7 queries (swept: 2^5..2^7
+                                       // per bucket within 2 %, 2^16 buckets -10 %)
+  if (const char* e = getenv(kind == 0 ? "WT_QSORT_A" : kind == 1 ? "WT_QSORT_R" : "WT_QSORT_S")) {
+    int a = 0, b = 0;  // tuning override "maxbits,log2 queries per bucket"
+    if (sscanf(e, "%d,%d", &a, &b) == 2 && a >= 10 && a <= (int)kQSortMaxBits && b >= 0 && b < 16) {
+      qmax = (u32)a;
+      qlog = (u32)b;
+    }
+  }
+  while (qb < qmax && (1ull << (qb + qlog)) < m) ++qb;
   u32 sym_bits = 0;
   if (kind != 0)
     while ((1u << sym_bits) < T.sigma) ++sym_bits;

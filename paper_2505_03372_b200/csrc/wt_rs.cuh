@@ -213,13 +213,25 @@ __device__ __forceinline__ u64 qselect(const QLevelDev& Q, u64 k) {
   const u64 j = (k - 1) >> kQSelLog;
   u64 lo = ld_u32_64b(sel + j);
   u64 hi = j + 1 < ns ? (u64)ld_u32_64b(sel + j + 1) : Q.n_lines - 1;
-  while (lo < hi) {  // last line whose count before it is below k
-    const u64 mid = (lo + hi + 1) >> 1;
+  // the answer is the last line in [lo, hi] whose count before it is below
+  // k: narrow by header probes to two candidates (dense bits: the samples are
+  // already at most one line apart), then load both lines at once -- one
+  // dependent step less than probing the second line's header first
+  while (lo + 1 < hi) {
+    const u64 mid = (lo + hi) >> 1;
     const u64 h = ld_u64_64b(reinterpret_cast<const u64*>(Q.lines + mid * kQLineU2));
     const u64 v = kOnes ? h : mid * kQBits - h;
     if (v < k) lo = mid; else hi = mid - 1;
   }
-  const QLine L = qload(Q, lo);
+  QLine L = qload(Q, lo);
+  if (hi > lo) {
+    const QLine B = qload(Q, hi);
+    const u64 v = kOnes ? B.hdr : hi * kQBits - B.hdr;
+    if (v < k) {
+      L = B;
+      lo = hi;
+    }
+  }
   k -= kOnes ? L.hdr : lo * kQBits - L.hdr;
   // find the word first (predicated selects), then ONE in-word select: inside
   // the loop it would run once per distinct word index in the warp

@@ -61,6 +61,17 @@ def main():
             bkey = ids_id * sub + ((a if kind == 1 else a - 1) >> shift)
             o2 = torch.argsort(bkey * (1 << 24) + torch.randint(0, 1 << 24, (m,), generator=g, device="cuda"))
             res.append(run(kind, syms[ids_id[o2]].contiguous(), a[o2].contiguous(), base))
+        # argument-block major, symbol minor (2^20 buckets): consecutive buckets
+        # are the same stretch of the text for every symbol
+        sarg = a if kind == 1 else a - 1
+        if kind == 2:  # ordinal -> approximate text position k * n / occ
+            sarg = (sarg.double() * n / occ[ids_id].double()).long()
+        shift = 0
+        while ((n - 1) >> shift) >= 4096:
+            shift += 1
+        bkey = (sarg >> shift) * 256 + ids_id
+        o3 = torch.argsort(bkey * (1 << 24) + torch.randint(0, 1 << 24, (m,), generator=g, device="cuda"))
+        res.append(run(kind, syms[ids_id[o3]].contiguous(), a[o3].contiguous(), base))
         t_plain = run(kind, syms[ids_id], a, base)
         # the cost of putting sorted-order results back in query order
         perm = o.to(torch.int64)
@@ -75,7 +86,7 @@ def main():
             if r >= 2:
                 ts.append(e0.elapsed_time(e1))
         print(f"{name:7s} F_SORT {t_sort:.3f} ms | presorted full {t_full:.3f} | by 2^16/2^20/2^24 buckets "
-              f"{res[0]:.3f} / {res[1]:.3f} / {res[2]:.3f} | unsorted {t_plain:.3f} | "
+              f"{res[0]:.3f} / {res[1]:.3f} / {res[2]:.3f} | pos-major 2^20 {res[3]:.3f} | unsorted {t_plain:.3f} | "
               f"unpermute (index_copy_) {np.median(ts):.3f}", flush=True)
 
 

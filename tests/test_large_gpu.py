@@ -208,3 +208,38 @@ def test_device_query_sort_unaligned_inputs(W):
                                       C.byref(bad), None))
     assert bad.value == -1
     assert np.array_equal(out.cpu().numpy(), W.rank_batch(t, ids[1:], pos[1:]))
+
+
+@pytest.mark.parametrize("name", ["u16_s4096", "u16_zipf_inferred", "u8_skewed", "dna"])
+def test_device_query_sort_other_trees(W, name):
+    """The sorted path on u16 / Zipf / skewed / DNA trees: bucket layouts with
+    many symbol bits (sigma up to 2^16) and select position estimates from very
+    unequal occurrence counts."""
+    text = LARGE[name]()
+    t = W.construct(text)
+    _, fr, fs = O.text_answers(text, 1 << (8 * text.dtype.itemsize))
+    r = np.random.default_rng(61)
+    m = 30011
+    pos = r.integers(0, len(text), m)
+    assert np.array_equal(W.access_batch(t, pos, sort=True), text[pos])
+    syms = t.alphabet.sorted_symbols[r.integers(0, t.sigma, m)].astype(np.int64)
+    p = r.integers(0, len(text) + 1, m)
+    assert np.array_equal(W.rank_batch(t, syms, p, sort=True), fr(syms, p))
+    occ = np.diff(t.cum_hist)
+    ids = np.flatnonzero(occ)[r.integers(0, np.count_nonzero(occ), m)]
+    ks = 1 + (r.random(m) * occ[ids]).astype(np.int64)
+    ss = t.alphabet.sorted_symbols[ids].astype(np.int64)
+    assert np.array_equal(W.select_batch(t, ss, ks, sort=True), fs(ss, ks))
+
+
+@pytest.mark.parametrize("m", [1, 2, 33, 4097])
+def test_device_query_sort_tiny_batches(W, m):
+    text = np.random.default_rng(71).integers(0, 256, 100003, dtype=np.uint8)
+    t = W.construct(text)
+    r = np.random.default_rng(72 + m)
+    pos = r.integers(0, len(text), m)
+    assert np.array_equal(W.access_batch(t, pos, sort=True), text[pos])
+    syms = t.alphabet.sorted_symbols[r.integers(0, t.sigma, m)].astype(np.int64)
+    ks = np.ones(m, np.int64)
+    _, _, fs = O.text_answers(text, 256)
+    assert np.array_equal(W.select_batch(t, syms, ks, sort=True), fs(syms, ks))

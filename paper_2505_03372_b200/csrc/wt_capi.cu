@@ -98,15 +98,11 @@ static int dalloc(T** p, size_t count, cudaStream_t st) {
 // O(sigma) planning (host): the reference's alphabet.py / wtree.py shape logic
 // ---------------------------------------------------------------------------
 static inline uint32_t ceil_log2_u(uint64_t s) {
-  uint32_t L = 0;
-  while ((1ull << L) < s) ++L;
-  return L;
+  return s <= 1 ? 0u : 64u - (uint32_t)__builtin_clzll(s - 1);
 }
-static inline uint64_t prev_pow_two_u(uint64_t x) {  // alphabet.py:28-32
+static inline uint64_t prev_pow_two_u(uint64_t x) {  // alphabet.py:28-32: largest 2^k < x
   if (x <= 2) return 1;
-  uint64_t p = 1;
-  while (p * 2 < x) p *= 2;
-  return p;
+  return 1ull << (63 - __builtin_clzll(x - 1));
 }
 
 struct Plan {
@@ -117,7 +113,8 @@ struct Plan {
   uint64_t n_words = 0;
   std::vector<NodeEnt> nodes;
   std::vector<uint64_t> node_off;  // start of level l in `nodes`
-  std::vector<std::vector<int64_t>> node_starts, node_rank0;
+  std::vector<uint64_t> n_nodes;                           // per level
+  std::vector<std::vector<int64_t>> node_starts, node_rank0;  // filled on export
   int code_bytes = 1;
 };
 
@@ -156,14 +153,68 @@ static void plan_codes(Plan& P) {
 }
 
 // hist (per id) known: cum_hist, level sizes, region layout, node tables.
+static std::vector<NodeEnt>& node_cache() {
+  static thread_local std::vector<NodeEnt> v;
+  return v;
+}
+// The node traversal (wtree.py:388-433): device node entries and per-level
+// node counts at build time; the reference's node_starts / node_rank0 arrays
+// only when exported (wt_tree_get), so a 2^16-symbol build does not allocate
+// them.
+static void plan_walk(Plan& P, bool tables) {
+  const uint32_t s = P.sigma, L = P.L;
+  static thread_local std::vector<std::pair<uint32_t, uint32_t>> cur, nxt;
+  cur.clear();
+  P.n_nodes.assign(L, 0);
+  if (tables) {
+    P.node_starts.assign(L, {});
+    P.node_rank0.assign(L, {});
+  }
+  if (L) cur.push_back({0, s});
+  for (uint32_t l = 0; l < L; ++l) {
+    int64_t zeros_before = 0;
+    nxt.clear();
+    P.n_nodes[l] = cur.size();
+    if (tables) {
+      P.node_starts[l].reserve(cur.size());
+      P.node_rank0[l].reserve(cur.size());
+    }
+    for (auto [a, b] : cur) {
+      const uint32_t p = (uint32_t)prev_pow_two_u(b - a);
+      const int64_t Z = P.cum[a + p] - P.cum[a];
+      if (tables) {
+        P.node_starts[l].push_back(a);
+        P.node_rank0[l].push_back(zeros_before);
+      } else {
+        const uint32_t key = (uint32_t)P.values[a] >> (L - l);
+        NodeEnt& ne = P.nodes[P.node_off[l] + key];
+        ne.zero_base = P.cum[a] - zeros_before;
+        ne.one_base = Z + zeros_before;
+        ne.leaf[0] = p == 1 ? (int)a : -1;
+        ne.leaf[1] = (b - a - p) == 1 ? (int)(a + p) : -1;
+      }
+      zeros_before += Z;
+      if (p >= 2) nxt.push_back({a, a + p});
+      if (b - a - p >= 2) nxt.push_back({a + p, b});
+    }
+    cur.swap(nxt);
+  }
+}
+
 static void plan_shape(Plan& P, uint32_t l2_bits) {
   (void)l2_bits;
   const uint32_t s = P.sigma, L = P.L;
   P.cum.assign(s + 1, 0);
   for (uint32_t i = 0; i < s; ++i) P.cum[i + 1] = P.cum[i] + P.hist[i];
+  // sizes[l] = symbols whose code is longer than l: by code length, O(sigma + L)
   P.sizes.assign(L, 0);
-  for (uint32_t i = 0; i < s; ++i)
-    for (uint32_t l = 0; l < P.lens[i]; ++l) P.sizes[l] += P.hist[i];
+  std::vector<int64_t> by_len(L + 1, 0);
+  for (uint32_t i = 0; i < s; ++i) by_len[P.lens[i]] += P.hist[i];
+  int64_t longer = 0;
+  for (uint32_t l = L; l-- > 0;) {
+    longer += by_len[l + 1];
+    P.sizes[l] = longer;
+  }
   P.offsets.assign(L, 0);
   uint64_t cursor = 0;
   for (uint32_t l = 0; l < L; ++l) {
@@ -174,32 +225,9 @@ static void plan_shape(Plan& P, uint32_t l2_bits) {
   // node tables, level by level (wtree.py:388-433); keys are code prefixes
   P.node_off.assign(L + 1, 0);
   for (uint32_t l = 0; l < L; ++l) P.node_off[l + 1] = P.node_off[l] + (1ull << l);
+  P.nodes.swap(node_cache());  // reuse the last build's pages (given back after the upload)
   P.nodes.assign(P.node_off[L], NodeEnt{0, 0, {-1, -1}});
-  P.node_starts.assign(L, {});
-  P.node_rank0.assign(L, {});
-  std::vector<std::pair<uint32_t, uint32_t>> cur, nxt;
-  if (L) cur.push_back({0, s});
-  for (uint32_t l = 0; l < L; ++l) {
-    int64_t zeros_before = 0;
-    nxt.clear();
-    for (auto [a, b] : cur) {
-      const uint32_t p = (uint32_t)prev_pow_two_u(b - a);
-      const uint32_t key = (uint32_t)P.values[a] >> (L - l);
-      const int64_t S = P.cum[a];
-      const int64_t Z = P.cum[a + p] - P.cum[a];
-      NodeEnt& ne = P.nodes[P.node_off[l] + key];
-      ne.zero_base = S - zeros_before;
-      ne.one_base = Z + zeros_before;
-      ne.leaf[0] = p == 1 ? (int)a : -1;
-      ne.leaf[1] = (b - a - p) == 1 ? (int)(a + p) : -1;
-      P.node_starts[l].push_back(a);
-      P.node_rank0[l].push_back(zeros_before);
-      zeros_before += Z;
-      if (p >= 2) nxt.push_back({a, a + p});
-      if (b - a - p >= 2) nxt.push_back({a + p, b});
-    }
-    cur.swap(nxt);
-  }
+  plan_walk(P, false);
   P.code_bytes = L <= 8 ? 1 : 2;
 }
 
@@ -240,6 +268,7 @@ struct wt_tree {
   cudaStream_t qstream[3] = {nullptr, nullptr, nullptr};  // copy-in, compute, copy-out
   cudaEvent_t qev[3][2] = {};                              // per stage and slot
   std::mutex qmutex;
+  std::mutex tables_mutex;  // lazy node_starts / node_rank0 (wt_tree_get)
   // build profile: [0] text upload + histogram + plan, [1 + l] level-l kernel (ms)
   std::vector<float> build_ms;
 };
@@ -309,7 +338,7 @@ static int alloc_tree(wt_tree* t, cudaStream_t st) {
     h.meta.n_bits = m;
     h.meta.n_l1 = (m + kL1Bits - 1) / kL1Bits;
     h.meta.n_l2 = (m + t->meta.l2_bits - 1) / t->meta.l2_bits;
-    h.meta.n_nodes = P.node_starts[l].size();
+    h.meta.n_nodes = P.n_nodes[l];
     TRY(dalloc(&h.l1, h.meta.n_l1, st));
     TRY(dalloc(&h.l2, h.meta.n_l2, st));
     TRY(dalloc(&h.ones, m / t->meta.sample_rate, st));
@@ -326,7 +355,10 @@ static int alloc_tree(wt_tree* t, cudaStream_t st) {
   TRY(dalloc(&t->symbols, P.sigma, st));
   TRY(dalloc(&t->sym2id, 65536, st));
   TRY(dalloc(&t->bad, 1, st));
-  std::vector<int> s2i(65536, -1);
+  // host temporaries reused across builds (thread-local): freshly mapped
+  // pages cost ~0.5 ms of page faults per 2^16-symbol build
+  static thread_local std::vector<int> s2i;
+  s2i.assign(65536, -1);
   for (uint32_t i = 0; i < P.sigma; ++i) s2i[P.symbols[i]] = (int)i;
   CU(cudaMemcpyAsync(t->sym2id, s2i.data(), 65536 * 4, cudaMemcpyHostToDevice, st));
   std::vector<u32> idc(P.sigma);
@@ -340,6 +372,8 @@ static int alloc_tree(wt_tree* t, cudaStream_t st) {
                      st));
   CU(cudaStreamSynchronize(st));  // host vectors above are temporaries
   uint64_t bytes = P.n_words * 8 + P.nodes.size() * sizeof(NodeEnt) + P.sigma * 14 + 8;
+  node_cache().swap(t->plan.nodes);  // the device holds the node table now
+  t->plan.nodes.clear();
   for (auto& h : t->lv)
     bytes += h.meta.n_l1 * 8 + h.meta.n_l2 * 2 + 2 * (h.meta.n_bits / t->meta.sample_rate) * 8 +
              h.n_lines * kQLineBytes + 2 * h.sel_cap * 4;
@@ -497,7 +531,8 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
     if (sym_bytes == 1 && (bm ? bm[0] == '1' : n_blk >= 2 * wlevel_warp_slots(sm_count(device))))
       TRY(S.get(&dbh, n_blk * 256));
     CU(launch_histogram(dtext, n, sym_bytes, dhist, sm_count(device), st, dbh));
-    std::vector<uint64_t> hraw(nb);
+    static thread_local std::vector<uint64_t> hraw;
+    hraw.assign(nb, 0);
     CU(cudaMemcpyAsync(hraw.data(), dhist, nb * 8, cudaMemcpyDeviceToHost, st));
     tr.mark("histogram launched");
     CU(cudaStreamSynchronize(st));
@@ -543,7 +578,9 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
     P.hist.assign(P.sigma, 0);
     for (uint32_t i = 0; i < P.sigma; ++i)
       if (P.symbols[i] < nb) P.hist[i] = (int64_t)hraw[P.symbols[i]];
+    tr.mark("alphabet done");
     plan_codes(P);
+    tr.mark("codes done");
     plan_shape(P, l2_bits);
     tr.mark("plan done");
 
@@ -573,7 +610,8 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
     tr.mark("tree allocated");
 
     // raw symbol -> code LUT for level 0, unless the map is the identity
-    std::vector<u16> lut(nb, 0);
+    static thread_local std::vector<u16> lut;
+    lut.assign(nb, 0);
     bool identity = true;
     for (uint32_t i = 0; i < P.sigma; ++i) {
       if (P.symbols[i] >= nb) continue;
@@ -835,9 +873,12 @@ extern "C" int wt_tree_get(const wt_tree* t, int what, uint32_t level, void* dst
     case WT_A_ZEROS:
       return copy_out(dst, t->lv[level].zeros, t->lv[level].meta.n_zeros * 8, cap, true);
     case WT_A_NODE_STARTS:
-      return copy_out(dst, P.node_starts[level].data(), P.node_starts[level].size() * 8, cap, false);
-    case WT_A_NODE_RANK0:
-      return copy_out(dst, P.node_rank0[level].data(), P.node_rank0[level].size() * 8, cap, false);
+    case WT_A_NODE_RANK0: {
+      std::lock_guard<std::mutex> lk(const_cast<wt_tree*>(t)->tables_mutex);
+      if (P.node_starts.size() != P.L) plan_walk(const_cast<Plan&>(P), true);
+      const auto& v = what == WT_A_NODE_STARTS ? P.node_starts[level] : P.node_rank0[level];
+      return copy_out(dst, v.data(), v.size() * 8, cap, false);
+    }
     default: return fail(WT_ERR_ARG, "unknown array selector");
   }
 }

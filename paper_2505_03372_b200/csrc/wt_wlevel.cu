@@ -1228,11 +1228,19 @@ template <typename TIn, typename TC, bool kLut>
 cudaError_t launch_w(const WLevelParams& p, int sms, cudaStream_t st) {
   const size_t smem = 512 + (size_t)W_WARPS * WF<TIn, TC>::WARP_SMEM;
   auto kern = wlevel_kernel<TIn, TC, kLut>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W_NT, smem);
-  if (per_sm < 1) per_sm = 1;
+  // attribute + occupancy once per device (host cost off the per-level path)
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int per_sm = dev >= 0 && dev < 64 ? cached[dev] : 0;
+  if (per_sm <= 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W_NT, smem);
+    if (per_sm < 1) per_sm = 1;
+    if (dev >= 0 && dev < 64) cached[dev] = per_sm;
+  }
   const u64 tiles = (p.m + WS<TIn>::TILE - 1) / WS<TIn>::TILE;
   if (!p.out) {  // the last level: no partition
     u64 blocks = (tiles + 7) / 8;

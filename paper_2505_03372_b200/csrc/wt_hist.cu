@@ -9,6 +9,7 @@
 // u8 : warp-private shared-memory sub-histograms (8 x 256 counters per CTA),
 //      16-byte streaming loads, one merge per CTA.
 // u16: CTA pairs split the alphabet in halves of 32768 u32 shared bins.
+#include <cstdlib>
 #include "wt_common.cuh"
 #include "wt_kernels.h"
 
@@ -146,6 +147,55 @@ __global__ void __launch_bounds__(H16_NT, 1) hist16_kernel(const u16* __restrict
     if (bins[i]) atomicAdd(&hist[half * 32768 + i], (u64)bins[i]);
 }
 
+// u16, one pass: each CTA counts ALL 65536 symbols of its chunks into packed
+// 16-bit shared counters (two per 32-bit word, 128 KB, one CTA per SM) and
+// reads its chunks once.  A 16-bit counter wrapping is seen in the atomic's
+// old value: the carry into the neighbouring counter is taken back and 65536
+// goes to the global bin instead.  Each CTA writes its counts as one row of
+// `part`; hist16_fold_kernel adds the rows.
+__global__ void __launch_bounds__(H16_NT, 1) hist16p_kernel(const u16* __restrict__ text, u64 n,
+                                                            u64* __restrict__ hist,
+                                                            u32* __restrict__ part) {
+  extern __shared__ u32 w2[];  // 32768 words = 65536 packed counters
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 32768; i += H16_NT) w2[i] = 0;
+  __syncthreads();
+  auto bump = [&](u32 a) {
+    const u32 sh = (a & 1u) * 16u;
+    const u32 old = atomicAdd(&w2[a >> 1], 1u << sh);
+    if (((old >> sh) & 0xffffu) == 0xffffu) {  // this counter wrapped
+      if (!sh) atomicSub(&w2[a >> 1], 1u << 16);
+      atomicAdd(&hist[a], 65536ull);
+    }
+  };
+  const u64 nvec = n >> 3;
+  const u64 stride = (u64)gridDim.x * H16_NT;
+  for (u64 v = (u64)blockIdx.x * H16_NT + tid; v < nvec; v += stride) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(text) + v);
+    const u32 w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      bump(w[i] & 0xffffu);
+      bump(w[i] >> 16);
+    }
+  }
+  if (blockIdx.x == 0)
+    for (u64 i = (nvec << 3) + tid; i < n; i += H16_NT) bump(text[i]);
+  __syncthreads();
+  u32* row = part + (u64)blockIdx.x * 65536;
+  for (int i = tid; i < 32768; i += H16_NT) {
+    const u32 x = w2[i];
+    reinterpret_cast<uint2*>(row)[i] = make_uint2(x & 0xffffu, x >> 16);
+  }
+}
+__global__ void hist16_fold_kernel(const u32* __restrict__ part, int rows, u64* __restrict__ hist) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= 65536) return;
+  u64 s = 0;
+  for (int r = 0; r < rows; ++r) s += part[(u64)r * 65536 + b];
+  if (s) hist[b] += s;
+}
+
 __global__ void __launch_bounds__(H_NT) first_outside_kernel(const void* __restrict__ text, u64 n,
                                                              int sym_bytes,
                                                              const u8* __restrict__ member,
@@ -173,7 +223,24 @@ cudaError_t launch_histogram(const void* text, u64 n, int sym_bytes, u64* hist, 
   if (blocks == 0) blocks = 1;
   if (sym_bytes == 1)
     hist8_kernel<<<(unsigned)blocks, H_NT, 0, st>>>((const u8*)text, n, hist);
-  else {
+  else if (!getenv("WT_HIST16_PAIRS")) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(hist16p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
+      attr = true;
+    }
+    u64 rows = (n / 8 + H16_NT - 1) / H16_NT;
+    if (rows > (u64)sms) rows = (u64)sms;
+    if (rows < 1) rows = 1;
+    u32* part = nullptr;
+    cudaError_t e = cudaMallocAsync(&part, rows * 65536 * 4, st);
+    if (e != cudaSuccess) return e;
+    hist16p_kernel<<<(unsigned)rows, H16_NT, 32768 * 4, st>>>((const u16*)text, n, hist, part);
+    hist16_fold_kernel<<<256, 256, 0, st>>>(part, (int)rows, hist);
+    e = cudaGetLastError();
+    cudaFreeAsync(part, st);
+    return e;
+  } else {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(hist16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);

@@ -243,3 +243,25 @@ def test_device_query_sort_tiny_batches(W, m):
     ks = np.ones(m, np.int64)
     _, _, fs = O.text_answers(text, 256)
     assert np.array_equal(W.select_batch(t, syms, ks, sort=True), fs(syms, ks))
+
+
+def test_hist16_counter_wrap(W):
+    """A hot symbol with far more than 65536 occurrences per CTA (the packed
+    16-bit shared counters wrap many times) next to rare ones and to the hot
+    counter's word neighbour: exact histogram, exact rank / select."""
+    r = np.random.default_rng(81)
+    n = (1 << 25) + 5
+    text = np.full(n, 40000, np.uint16)
+    text[r.integers(0, n, 50000)] = r.integers(0, 65536, 50000).astype(np.uint16)
+    text[r.integers(0, n, 7)] = 40001
+    t = W.construct(text)
+    vals, cnts = np.unique(text, return_counts=True)
+    assert np.array_equal(t.alphabet.sorted_symbols, vals)
+    assert np.array_equal(np.diff(t.cum_hist), cnts)
+    _, fr, fs = O.text_answers(text, 65536)
+    syms = np.array([40000, 40001, int(vals[0]), int(vals[-1])] * 250, np.int64)
+    pos = r.integers(0, n + 1, len(syms))
+    assert np.array_equal(W.rank_batch(t, syms, pos), fr(syms, pos))
+    occ = dict(zip(vals.tolist(), cnts.tolist()))
+    ks = 1 + (r.random(len(syms)) * np.array([occ[int(s_)] for s_ in syms])).astype(np.int64)
+    assert np.array_equal(W.select_batch(t, syms, ks), fs(syms, ks))

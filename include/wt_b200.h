@@ -71,10 +71,12 @@ extern "C" {
                                *bad_index = first invalid query or -1           */
 #define WT_F_ACCESS_IDS  4  /* access returns int64 minimal ids (access_ids_bulk)
                                instead of decoded symbols (batch._decode)        */
-#define WT_F_SORT        8  /* sort the batch on the device by (symbol, coarse
-                               position / ordinal) before the walk, for locality
-                               (batch.sort_queries_by_symbol, batch.py:61-75;
-                               PAPER.md:928, :988); results stay in query order */
+#define WT_F_SORT        8  /* sort the batch on the device before the walk, for
+                               locality -- the device counterpart of
+                               batch.sort_queries_by_symbol (batch.py:61-75;
+                               PAPER.md:928, :988): buckets of (coarse text
+                               position, symbol); results stay in query order,
+                               errors report the first bad index as unsorted  */
 
 /* array selectors for wt_tree_get */
 #define WT_A_SYMBOLS      0   /* u16[sigma]   sorted alphabet symbols        */

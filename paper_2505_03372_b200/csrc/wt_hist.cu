@@ -149,10 +149,9 @@ __global__ void __launch_bounds__(H16_NT, 1) hist16_kernel(const u16* __restrict
 
 // u16, one pass: each CTA counts ALL 65536 symbols of its chunks into packed
 // 16-bit shared counters (two per 32-bit word, 128 KB, one CTA per SM) and
-// reads its chunks once.  A 16-bit counter wrapping is seen in the atomic's
-// old value: the carry into the neighbouring counter is taken back and 65536
-// goes to the global bin instead.  Each CTA writes its counts as one row of
-// `part`; hist16_fold_kernel adds the rows.
+// reads its chunks once.  Counters spill 32768 to the global bin before they
+// could carry into their neighbour (see `bump`).  Each CTA writes its counts
+// as one row of `part`; hist16_fold_kernel adds the rows.
 __global__ void __launch_bounds__(H16_NT, 1) hist16p_kernel(const u16* __restrict__ text, u64 n,
                                                             u64* __restrict__ hist,
                                                             u32* __restrict__ part) {
@@ -160,12 +159,17 @@ __global__ void __launch_bounds__(H16_NT, 1) hist16p_kernel(const u16* __restric
   const int tid = threadIdx.x;
   for (int i = tid; i < 32768; i += H16_NT) w2[i] = 0;
   __syncthreads();
+  // Each 16-bit field counts up to 0x7fff with bit 15 as a guard: the one
+  // increment that takes a field from 0x7fff to 0x8000 (seen in the old value)
+  // clears the guard again and moves 32768 to the global bin.  Increments
+  // landing in between only raise the field above 0x8000, so no carry ever
+  // reaches the neighbouring counter.
   auto bump = [&](u32 a) {
     const u32 sh = (a & 1u) * 16u;
     const u32 old = atomicAdd(&w2[a >> 1], 1u << sh);
-    if (((old >> sh) & 0xffffu) == 0xffffu) {  // this counter wrapped
-      if (!sh) atomicSub(&w2[a >> 1], 1u << 16);
-      atomicAdd(&hist[a], 65536ull);
+    if (((old >> sh) & 0xffffu) == 0x7fffu) {
+      atomicSub(&w2[a >> 1], 0x8000u << sh);
+      atomicAdd(&hist[a], 32768ull);
     }
   };
   const u64 nvec = n >> 3;

@@ -246,14 +246,16 @@ def test_device_query_sort_tiny_batches(W, m):
 
 
 def test_hist16_counter_wrap(W):
-    """A hot symbol with far more than 65536 occurrences per CTA (the packed
-    16-bit shared counters wrap many times) next to rare ones and to the hot
-    counter's word neighbour: exact histogram, exact rank / select."""
+    """Hot symbols with far more than 32768 occurrences per CTA (the packed
+    16-bit shared counters spill many times), two of them in the same counter
+    word, next to rare ones: exact histogram, exact rank / select."""
     r = np.random.default_rng(81)
     n = (1 << 25) + 5
-    text = np.full(n, 40000, np.uint16)
+    # two hot symbols sharing one 32-bit counter word (40000, 40001) and a
+    # third hot one, each far past 32768 per CTA
+    text = np.where(r.random(n) < 0.5, 40000, 40001).astype(np.uint16)
+    text[r.integers(0, n, n // 5)] = 7
     text[r.integers(0, n, 50000)] = r.integers(0, 65536, 50000).astype(np.uint16)
-    text[r.integers(0, n, 7)] = 40001
     t = W.construct(text)
     vals, cnts = np.unique(text, return_counts=True)
     assert np.array_equal(t.alphabet.sorted_symbols, vals)

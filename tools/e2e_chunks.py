@@ -28,7 +28,8 @@ def main():
     ssym = pin(syms[sid])
     ks = pin(torch.minimum(1 + (torch.rand(m, generator=g, device="cuda", dtype=torch.float64)
                                 * occ[sid]).long(), occ[sid]))
-    for log in (16, 18, 20, 21, 22):
+    logs = [int(x) for x in os.environ.get("E2E_LOGS", "16,18,20,21,22").split(",")]
+    for log in logs:
         c = 1 << log
         for srt in (False, True):
             ts = []

@@ -22,7 +22,22 @@ for name, f in (("h2d", lambda: y.copy_(x, non_blocking=True)), ("d2h", lambda: 
         f()
     torch.cuda.synchronize()
     print(f"{name}: {3 * (1 << 30) / (time.perf_counter() - t0) / 1e9:.1f} GB/s")
-del x, y
+# both directions at once (two streams): the e2e step moves 1.33 GB in and
+# 0.57 GB out concurrently
+x2 = torch.empty(1 << 29, dtype=torch.uint8).pin_memory()
+y2 = torch.empty(1 << 29, dtype=torch.uint8, device=dev)
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(3):
+    with torch.cuda.stream(s1):
+        y.copy_(x, non_blocking=True)
+    with torch.cuda.stream(s2):
+        x2.copy_(y2, non_blocking=True)
+torch.cuda.synchronize()
+dt = time.perf_counter() - t0
+print(f"h2d 1 GiB + d2h 0.5 GiB concurrently: {3 * 1.5 * (1 << 30) / dt / 1e9:.1f} GB/s combined")
+del x, y, x2, y2
 n = 1 << 30
 text = np.random.default_rng(0).integers(0, 256, n, dtype=np.uint8)
 tree = W.construct(torch.from_numpy(text).to(dev))

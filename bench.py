@@ -322,6 +322,9 @@ def run_ours(args):
                "h2d_bytes_per_step": int(per[0] * 8 + (per[1] + per[2]) * 16),
                "d2h_bytes_per_step": int(per[0] * 1 + (per[1] + per[2]) * 8),
                "api": "access_batch / rank_batch / select_batch on pinned numpy arrays"}
+        # the bound: PCIe traffic, both directions at once (~70 GB/s measured on
+        # the box, tools/e2e_probe.py)
+        e2e["pcie_GB_per_s"] = (e2e["h2d_bytes_per_step"] + e2e["d2h_bytes_per_step"]) / (e2e_ms / 1e3) / 1e9
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -8,7 +8,7 @@
 //
 // u8 : warp-private shared-memory sub-histograms (8 x 256 counters per CTA),
 //      16-byte streaming loads, one merge per CTA.
-// u16: CTA pairs split the alphabet in halves of 32768 u32 shared bins.
+// u16: one CTA per SM, packed 16-bit shared counters for all 65536 symbols.
 #include <cstdlib>
 #include "wt_common.cuh"
 #include "wt_kernels.h"
@@ -112,41 +112,7 @@ __global__ void __launch_bounds__(256) block_l1_kernel(const u32* __restrict__ b
   }
 }
 
-// u16: CTAs work in pairs over the same chunks of the text; CTA 2k counts
-// symbols < 32768 and CTA 2k+1 the rest, each into 32768 u32 shared bins
-// (128 KB, one CTA per SM).  The pair reads each chunk at about the same
-// time, so the second read is mostly an L2 hit.
 constexpr int H16_NT = 1024;
-__global__ void __launch_bounds__(H16_NT, 1) hist16_kernel(const u16* __restrict__ text, u64 n,
-                                                           u64* __restrict__ hist) {
-  extern __shared__ u32 bins[];  // 32768
-  const int tid = threadIdx.x;
-  const u32 half = blockIdx.x & 1u;
-  const u64 pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  for (int i = tid; i < 32768; i += H16_NT) bins[i] = 0;
-  __syncthreads();
-  const u64 nvec = n >> 3;
-  const u64 stride = npairs * H16_NT;
-  for (u64 v = pair * H16_NT + tid; v < nvec; v += stride) {
-    const uint4 q = __ldg(reinterpret_cast<const uint4*>(text) + v);
-    const u32 w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const u32 a = w[i] & 0xffffu, c = w[i] >> 16;
-      if ((a >> 15) == half) atomicAdd(&bins[a & 32767u], 1u);
-      if ((c >> 15) == half) atomicAdd(&bins[c & 32767u], 1u);
-    }
-  }
-  if (pair == 0)
-    for (u64 i = (nvec << 3) + tid; i < n; i += H16_NT) {
-      const u32 a = text[i];
-      if ((a >> 15) == half) atomicAdd(&bins[a & 32767u], 1u);
-    }
-  __syncthreads();
-  for (int i = tid; i < 32768; i += H16_NT)
-    if (bins[i]) atomicAdd(&hist[half * 32768 + i], (u64)bins[i]);
-}
-
 // u16, one pass: each CTA counts ALL 65536 symbols of its chunks into packed
 // 16-bit shared counters (two per 32-bit word, 128 KB, one CTA per SM) and
 // reads its chunks once.  Counters spill 32768 to the global bin before they
@@ -227,7 +193,7 @@ cudaError_t launch_histogram(const void* text, u64 n, int sym_bytes, u64* hist, 
   if (blocks == 0) blocks = 1;
   if (sym_bytes == 1)
     hist8_kernel<<<(unsigned)blocks, H_NT, 0, st>>>((const u8*)text, n, hist);
-  else if (!getenv("WT_HIST16_PAIRS")) {
+  else {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(hist16p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
@@ -244,16 +210,6 @@ cudaError_t launch_histogram(const void* text, u64 n, int sym_bytes, u64* hist, 
     e = cudaGetLastError();
     cudaFreeAsync(part, st);
     return e;
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(hist16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
-      attr = true;
-    }
-    u64 b16 = 2 * ((n / 8 + H16_NT - 1) / H16_NT);
-    if (b16 > (u64)(sms & ~1)) b16 = (u64)(sms & ~1);
-    if (b16 < 2) b16 = 2;
-    hist16_kernel<<<(unsigned)b16, H16_NT, 32768 * 4, st>>>((const u16*)text, n, hist);
   }
   return cudaGetLastError();
 }

@@ -72,9 +72,11 @@ class BatchRunner:
 
     def __init__(self, tree: WaveletTree, chunk_size: int = DEFAULT_CHUNK_SIZE,
                  workers: int = 1, *, sort: bool = False):
-        """``sort=True`` (extension): each chunk is sorted on the device by
-        symbol and coarse position before the walk (the paper's query sorting,
-        PAPER.md:928, :988); results stay in query order."""
+        """``sort=True`` (extension): each chunk is sorted on the device into
+        buckets of (coarse text position, symbol) before the walk -- the
+        device counterpart of `sort_queries_by_symbol` (the paper's query
+        sorting); results stay in query order and errors
+        report the first bad index of the unsorted batch."""
         if chunk_size < 1:
             raise ValueError("chunk_size must be positive")
         self.tree = tree

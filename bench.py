@@ -297,6 +297,12 @@ def run_ours(args):
                 "frac": dom_q["model_GB_per_s"] / hbm, "peak_source": peak_kind,
                 "traffic": traffic_from_profiles(f"{dom}_kernel", per[["access", "rank",
                                                                         "select"].index(dom)])}
+    if roofline["traffic"]:
+        # what the DRAM actually moved for this kind (ncu, profiles/ncu_traffic.json)
+        roofline["dram_frac"] = roofline["traffic"] / (dom_q["ms"] / 1e3) / 1e9 / hbm
+    roofline["note"] = ("achieved = SURVEY 8(d) sector-model bytes (every step one DRAM sector) / "
+                        "the kind's batch time incl. the device sort; sorted batches reuse sectors "
+                        "in L2, so frac can pass 1 -- dram_frac is the measured DRAM share")
 
     # ---------------- end to end through the public API -------------------------
     e2e = None

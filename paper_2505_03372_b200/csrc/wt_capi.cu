@@ -528,8 +528,12 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
     u32* dbh = nullptr;
     // (WT_BLOCK_MODE=0|1 forces it off / on: the parity tests run both)
     const char* bm = getenv("WT_BLOCK_MODE");
-    if (sym_bytes == 1 && (bm ? bm[0] == '1' : n_blk >= 2 * wlevel_warp_slots(sm_count(device))))
-      TRY(S.get(&dbh, n_blk * 256));
+    const bool want_blocks = bm ? bm[0] == '1' : n_blk >= 2 * wlevel_warp_slots(sm_count(device));
+    if (want_blocks && sym_bytes == 1) TRY(S.get(&dbh, n_blk * 256));
+    if (want_blocks && sym_bytes == 2) {  // level 0 in block mode when its threshold is 32768
+      TRY(S.get(&dbh, n_blk + 4));
+      CU(cudaMemsetAsync(dbh, 0, (n_blk + 4) * 4, st));
+    }
     CU(launch_histogram(dtext, n, sym_bytes, dhist, sm_count(device), st, dbh));
     static thread_local std::vector<uint64_t> hraw;
     hraw.assign(nb, 0);
@@ -672,11 +676,13 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
           thr = P.symbols[i];
           break;
         }
-      const bool block_mode = dbh && P.L >= 2;
+      const bool block_mode = dbh && P.L >= 2 && (sym_bytes == 1 || thr == 32768u);
       if (P.L && P.sizes[0]) {
         CU(cudaMemsetAsync(l1cnt[0], 0, (t->lv[0].meta.n_l1 + 4) * 4, st));
-        if (block_mode)
+        if (block_mode && sym_bytes == 1)
           CU(launch_block_l1(dbh, n_blk, thr, l1cnt[0], st));
+        else if (block_mode)  // u16: K1 counted the symbols >= 32768 per block
+          CU(cudaMemcpyAsync(l1cnt[0], dbh, n_blk * 4, cudaMemcpyDeviceToDevice, st));
         else
           CU(launch_wcount0(dtext, n, sym_bytes, thr, tcnt[0], l1cnt[0], sm_count(device), st));
       }

@@ -120,7 +120,8 @@ constexpr int H16_NT = 1024;
 // as one row of `part`; hist16_fold_kernel adds the rows.
 __global__ void __launch_bounds__(H16_NT, 1) hist16p_kernel(const u16* __restrict__ text, u64 n,
                                                             u64* __restrict__ hist,
-                                                            u32* __restrict__ part) {
+                                                            u32* __restrict__ part,
+                                                            u32* __restrict__ block_hi) {
   extern __shared__ u32 w2[];  // 32768 words = 65536 packed counters
   const int tid = threadIdx.x;
   for (int i = tid; i < 32768; i += H16_NT) w2[i] = 0;
@@ -140,17 +141,32 @@ __global__ void __launch_bounds__(H16_NT, 1) hist16p_kernel(const u16* __restric
   };
   const u64 nvec = n >> 3;
   const u64 stride = (u64)gridDim.x * H16_NT;
-  for (u64 v = (u64)blockIdx.x * H16_NT + tid; v < nvec; v += stride) {
-    const uint4 q = __ldg(reinterpret_cast<const uint4*>(text) + v);
-    const u32 w[4] = {q.x, q.y, q.z, q.w};
+  // warp-uniform trip count (the per-block reduction below needs every lane)
+  for (u64 wv = (u64)blockIdx.x * H16_NT + (tid & ~31); wv < nvec; wv += stride) {
+    const u64 v = wv + (tid & 31);
+    uint4 q = make_uint4(0, 0, 0, 0);
+    if (v < nvec) {
+      q = __ldg(reinterpret_cast<const uint4*>(text) + v);
+      const u32 w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      bump(w[i] & 0xffffu);
-      bump(w[i] >> 16);
+      for (int i = 0; i < 4; ++i) {
+        bump(w[i] & 0xffffu);
+        bump(w[i] >> 16);
+      }
+    }
+    if (block_hi) {  // symbols >= 32768 per L1 block: a warp's 256 symbols share one block
+      u32 hi = (u32)(__popc(q.x & 0x80008000u) + __popc(q.y & 0x80008000u)) +
+               (u32)(__popc(q.z & 0x80008000u) + __popc(q.w & 0x80008000u));
+#pragma unroll
+      for (int d = 16; d; d >>= 1) hi += __shfl_xor_sync(0xffffffffu, hi, d);
+      if ((tid & 31) == 0 && hi) atomicAdd(block_hi + ((wv << 3) >> 16), hi);
     }
   }
   if (blockIdx.x == 0)
-    for (u64 i = (nvec << 3) + tid; i < n; i += H16_NT) bump(text[i]);
+    for (u64 i = (nvec << 3) + tid; i < n; i += H16_NT) {
+      bump(text[i]);
+      if (block_hi && text[i] >= 32768u) atomicAdd(block_hi + (i >> 16), 1u);
+    }
   __syncthreads();
   u32* row = part + (u64)blockIdx.x * 65536;
   for (int i = tid; i < 32768; i += H16_NT) {
@@ -205,7 +221,8 @@ cudaError_t launch_histogram(const void* text, u64 n, int sym_bytes, u64* hist, 
     u32* part = nullptr;
     cudaError_t e = cudaMallocAsync(&part, rows * 65536 * 4, st);
     if (e != cudaSuccess) return e;
-    hist16p_kernel<<<(unsigned)rows, H16_NT, 32768 * 4, st>>>((const u16*)text, n, hist, part);
+    hist16p_kernel<<<(unsigned)rows, H16_NT, 32768 * 4, st>>>((const u16*)text, n, hist, part,
+                                                              block_hist);
     hist16_fold_kernel<<<256, 256, 0, st>>>(part, (int)rows, hist);
     e = cudaGetLastError();
     cudaFreeAsync(part, st);

@@ -43,8 +43,9 @@ cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, u32 thr, u32* 
 cudaError_t launch_l1_scan(const u32* counts, u64 n_l1, u64* l1, u64* total, cudaStream_t st);
 
 // K1: raw-symbol histogram (wt_hist.cu); hist must be zeroed (u64[256|65536])
-// block_hist (u8 only, may be null): also the 256-bin histogram of every
-// 65536-symbol L1 block, u32[n_blocks][256]
+// block_hist (may be null): per 65536-symbol L1 block, u8: its 256-bin
+// histogram, u32[n_blocks][256]; u16: its count of symbols >= 32768,
+// u32[n_blocks] (zeroed by the caller)
 cudaError_t launch_histogram(const void* text, u64 n, int sym_bytes, u64* hist, int sms,
                              cudaStream_t st, u32* block_hist = nullptr);
 // first text position whose raw symbol has member[sym] == 0; *best preset to ~0

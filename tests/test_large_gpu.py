@@ -267,3 +267,29 @@ def test_hist16_counter_wrap(W):
     occ = dict(zip(vals.tolist(), cnts.tolist()))
     ks = 1 + (r.random(len(syms)) * np.array([occ[int(s_)] for s_ in syms])).astype(np.int64)
     assert np.array_equal(W.select_batch(t, syms, ks), fs(syms, ks))
+
+
+@pytest.mark.parametrize("case", ["full", "declared_zipf", "s4096_fallback", "partial_blocks"])
+def test_level0_block_mode_u16(W, case, monkeypatch):
+    """u16 level 0 in block mode: K1 counts the symbols >= 32768 per L1 block,
+    used when the top-bit threshold is 32768 (full or declared 2^16
+    alphabets); other thresholds fall back to the counting pass."""
+    monkeypatch.setenv("WT_BLOCK_MODE", "1")
+    r = np.random.default_rng(91)
+    alpha = None
+    if case == "full":
+        text = r.integers(0, 65536, (1 << 21) + 3).astype(np.uint16)
+    elif case == "declared_zipf":
+        text = _zipf((1 << 21) + 7, 65536, seed=13)
+        alpha = np.arange(65536, dtype=np.uint16)
+    elif case == "s4096_fallback":
+        text = r.integers(0, 4096, (1 << 21) + 1).astype(np.uint16)
+    else:
+        text = r.integers(0, 65536, 3 * 65536 + 999).astype(np.uint16)
+        alpha = np.arange(65536, dtype=np.uint16)
+    if alpha is None:
+        t, o = W.construct(text), O.build(text)
+    else:
+        t, o = W.construct_with_alphabet(text, alpha), O.build_with_alphabet(text, alpha)
+    assert_same_structure(t, o)
+    _check_queries(W, t, text, t.alphabet.sorted_symbols if alpha is None else alpha, m=4000)

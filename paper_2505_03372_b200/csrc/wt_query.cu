@@ -40,11 +40,12 @@ __global__ void __launch_bounds__(Q_NT) access_kernel(const __grid_constant__ Tr
                                                       const i64* __restrict__ pos,
                                                       void* __restrict__ out, u64 m, u64 base,
                                                       u64* __restrict__ bad,
-                                                      bool packed) {
+                                                      bool packed,
+                                                      const u32* __restrict__ pos32 = nullptr) {
   const u64 q = (u64)blockIdx.x * Q_NT + threadIdx.x;
   if (q >= m) return;
   const u64 i = q;
-  u64 p = (u64)ld_stream_i64(pos + q, l2_evict_first_policy());
+  u64 p = pos32 ? (u64)__ldg(pos32 + q) : (u64)ld_stream_i64(pos + q, l2_evict_first_policy());
   if (packed) p = min(p & ((1ull << 48) - 1), T.n - 1);  // sorted batch: clamped in range
   if (kValidate && p >= T.n) {  // negative positions wrap to huge values
     atomicMin(bad, base + i);
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restri
                                                              const i64* __restrict__ args, u64 m,
                                                              u32* __restrict__ cursor,
                                                              i64* __restrict__ sargs,
+                                                             u32* __restrict__ sargs32,
                                                              u32* __restrict__ slot_of) {
   const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
   if (i >= m) return;
@@ -353,8 +355,12 @@ __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restri
                : "=l"(a) : "l"(args + i), "l"(pf));
   a &= (1ull << 48) - 1;
   const u64 v = with_id ? a | ((u64)(b & ((1u << sym_bits) - 1u)) << 48) : a;
-  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(sargs + slot), "l"(v), "l"(pl)
-               : "memory");
+  if (sargs32)  // access on a text below 2^32 symbols: 4-byte records
+    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(sargs32 + slot), "r"((u32)v),
+                 "l"(pl) : "memory");
+  else
+    asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(sargs + slot), "l"(v), "l"(pl)
+                 : "memory");
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(slot_of + i),
                "r"(slot), "l"(pf) : "memory");
 }
@@ -414,16 +420,31 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   u32* partial = S.hist + (1u << kQSortMaxBits);
   qsort_scan_partial_kernel<<<sb, 1024, 0, st>>>(S.hist, nb, partial);
   qsort_scan_final_kernel<<<sb, 1024, 0, st>>>(S.hist, nb, partial);
+  // access on texts below 2^32: the sorted positions as 4-byte records (half
+  // the scattered bytes; the sorted_args buffer holds them)
+  u32* s32 = kind == 0 && T.n <= 0xffffffffull ? reinterpret_cast<u32*>(S.sorted_args) : nullptr;
   qsort_scatter_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(S.bucket_of, kind != 0, sym_bits,
-                                                          args, m, S.hist, S.sorted_args, S.slot_of);
+                                                          args, m, S.hist, S.sorted_args, s32,
+                                                          S.slot_of);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // ids are mapped minimal ids now (packed into the arguments): run
   // unvalidated -- validation happened above; invalid queries are clamped
   // into range by the walk and the batch raises anyway.  Results land in
   // sorted order (coalesced), then one gather puts them in query order.
-  e = launch_query(T, kind, out_kind, false, nullptr, S.sorted_args, S.res, m, rate_log, base, bad,
-                   st, true);
+  if (s32) {
+    const unsigned qb2 = (unsigned)((m + Q_NT - 1) / Q_NT);
+    if (out_kind == 8)
+      access_kernel<8, false><<<qb2, Q_NT, 0, st>>>(T, nullptr, S.res, m, base, bad, true, s32);
+    else if (out_kind == 1)
+      access_kernel<1, false><<<qb2, Q_NT, 0, st>>>(T, nullptr, S.res, m, base, bad, true, s32);
+    else
+      access_kernel<2, false><<<qb2, Q_NT, 0, st>>>(T, nullptr, S.res, m, base, bad, true, s32);
+    e = cudaGetLastError();
+  } else {
+    e = launch_query(T, kind, out_kind, false, nullptr, S.sorted_args, S.res, m, rate_log, base,
+                     bad, st, true);
+  }
   if (e != cudaSuccess) return e;
   const unsigned ub = (unsigned)((m + 4 * Q_NT - 1) / (4 * Q_NT));
   const int ob = kind == 0 ? out_kind : 8;

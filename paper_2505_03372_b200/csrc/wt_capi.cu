@@ -268,7 +268,8 @@ struct wt_tree {
   cudaStream_t qstream[3] = {nullptr, nullptr, nullptr};  // copy-in, compute, copy-out
   cudaEvent_t qev[3][2] = {};                              // per stage and slot
   std::mutex qmutex;
-  std::mutex tables_mutex;  // lazy node_starts / node_rank0 (wt_tree_get)
+  std::mutex tables_mutex;
+  u32 sel_kbits = 0;        // select_kbits() cache  // lazy node_starts / node_rank0 (wt_tree_get)
   // build profile: [0] text upload + histogram + plan, [1 + l] level-l kernel (ms)
   std::vector<float> build_ms;
 };
@@ -905,6 +906,17 @@ extern "C" int wt_tree_destroy(wt_tree* t) {
 // ---------------------------------------------------------------------------
 // queries
 // ---------------------------------------------------------------------------
+// bits of the largest select ordinal (k <= max occurrences), cached per tree
+static u32 select_kbits(wt_tree* t) {
+  if (!t->sel_kbits) {
+    u64 mx = 1;
+    for (uint32_t i = 0; i < t->plan.sigma; ++i)
+      mx = std::max<u64>(mx, (u64)(t->plan.cum[i + 1] - t->plan.cum[i]));
+    t->sel_kbits = ceil_log2_u(mx + 1);
+  }
+  return t->sel_kbits;
+}
+
 extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int64_t* args,
                              void* out, uint64_t m, uint64_t chunk, int flags, void* stream,
                              int64_t* bad_index, float* ms_out) {
@@ -934,6 +946,7 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
       const uint64_t slice = std::min<uint64_t>(m, 1ull << 31);
       Scratch S{{}, st};
       QuerySortScratch Q{};
+      Q.sel_kbits = select_kbits(t);
       TRY(S.get(&Q.hist, (1u << kQSortMaxBits) + 256));
       TRY(S.get(&Q.bucket_of, slice));
       TRY(S.get(&Q.sorted_args, slice));
@@ -1025,6 +1038,7 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
     } else if (e == cudaSuccess) {
       u8* sp = (u8*)(((uintptr_t)(d_out + chunk * out_elem) + 15) & ~(uintptr_t)15);
       QuerySortScratch Q{};
+      Q.sel_kbits = select_kbits(t);
       auto take = [&](size_t bytes) {
         u8* p = sp;
         sp = (u8*)(((uintptr_t)(sp + bytes) + 15) & ~(uintptr_t)15);

@@ -69,6 +69,7 @@ struct QuerySortScratch {
   i64* sorted_args; // m: argument | id << 48
   u32* slot_of;     // m: sorted slot of each query (query order)
   void* res;        // m results in sorted order (out_kind bytes each)
+  u32 sel_kbits = 0; // bits of the largest select ordinal (0: 8-byte records only)
 };
 cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool validate,
                                 const i64* ids, const i64* args, void* out, u64 m, int rate_log,

@@ -131,16 +131,24 @@ __global__ void __launch_bounds__(Q_NT) select_kernel(const __grid_constant__ Tr
                                                       const i64* __restrict__ ks,
                                                       i64* __restrict__ out, u64 m, int rate_log,
                                                       u64 base, u64* __restrict__ bad,
-                                                      bool packed) {
+                                                      bool packed,
+                                                      const u32* __restrict__ ks32 = nullptr,
+                                                      u32 kbits = 0) {
   const u64 q = (u64)blockIdx.x * Q_NT + threadIdx.x;
   if (q >= m) return;
   const u64 i = q;
   u32 c;
   i64 k;
   const u64 pol = l2_evict_first_policy();
-  if (packed) {  // sorted batch: packed (ordinal | id << 48), clamped in range
+  if (packed) {  // sorted batch: packed (ordinal | id << 48 or << kbits), clamped in range
     u64 a;
-    qsort_unpack(ld_stream_i64(ks + q, pol), c, a);
+    if (ks32) {
+      const u32 v = __ldg(ks32 + q);
+      c = v >> kbits;
+      a = v & ((1u << kbits) - 1u);
+    } else {
+      qsort_unpack(ld_stream_i64(ks + q, pol), c, a);
+    }
     const i64 occ = __ldg(T.cum + c + 1) - __ldg(T.cum + c);
     k = min(max((i64)a, (i64)1), max(occ, (i64)1));
   } else if (k = ks[q], !symbol_id<kValidate>(T, ids[q], c) ||
@@ -335,7 +343,7 @@ __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restri
                                                              const i64* __restrict__ args, u64 m,
                                                              u32* __restrict__ cursor,
                                                              i64* __restrict__ sargs,
-                                                             u32* __restrict__ sargs32,
+                                                             u32* __restrict__ sargs32, u32 kbits,
                                                              u32* __restrict__ slot_of) {
   const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
   if (i >= m) return;
@@ -355,9 +363,13 @@ __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restri
                : "=l"(a) : "l"(args + i), "l"(pf));
   a &= (1ull << 48) - 1;
   const u64 v = with_id ? a | ((u64)(b & ((1u << sym_bits) - 1u)) << 48) : a;
-  if (sargs32)  // access on a text below 2^32 symbols: 4-byte records
-    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(sargs32 + slot), "r"((u32)v),
+  if (sargs32) {  // 4-byte records: access position, or select (ordinal | id << kbits)
+    // (invalid queries -- the batch raises -- keep a masked ordinal and id 0)
+    const u32 v32 = with_id ? ((u32)a & ((1u << kbits) - 1u)) | ((b & ((1u << sym_bits) - 1u)) << kbits)
+                            : (u32)a;
+    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(sargs32 + slot), "r"(v32),
                  "l"(pl) : "memory");
+  }
   else
     asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(sargs + slot), "l"(v), "l"(pl)
                  : "memory");
@@ -422,17 +434,24 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   qsort_scan_final_kernel<<<sb, 1024, 0, st>>>(S.hist, nb, partial);
   // access on texts below 2^32: the sorted positions as 4-byte records (half
   // the scattered bytes; the sorted_args buffer holds them)
-  u32* s32 = kind == 0 && T.n <= 0xffffffffull ? reinterpret_cast<u32*>(S.sorted_args) : nullptr;
+  // select when ordinal and id fit 32 bits together: (ordinal | id << kbits)
+  const bool sel32 = kind == 2 && S.sel_kbits && S.sel_kbits + sym_bits <= 32;
+  u32* s32 = (kind == 0 && T.n <= 0xffffffffull) || sel32 ? reinterpret_cast<u32*>(S.sorted_args)
+                                                          : nullptr;
   qsort_scatter_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(S.bucket_of, kind != 0, sym_bits,
                                                           args, m, S.hist, S.sorted_args, s32,
-                                                          S.slot_of);
+                                                          sel32 ? S.sel_kbits : 0u, S.slot_of);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // ids are mapped minimal ids now (packed into the arguments): run
   // unvalidated -- validation happened above; invalid queries are clamped
   // into range by the walk and the batch raises anyway.  Results land in
   // sorted order (coalesced), then one gather puts them in query order.
-  if (s32) {
+  if (sel32) {
+    select_kernel<false><<<(unsigned)((m + Q_NT - 1) / Q_NT), Q_NT, 0, st>>>(
+        T, nullptr, nullptr, (i64*)S.res, m, rate_log, base, bad, true, s32, S.sel_kbits);
+    e = cudaGetLastError();
+  } else if (s32) {
     const unsigned qb2 = (unsigned)((m + Q_NT - 1) / Q_NT);
     if (out_kind == 8)
       access_kernel<8, false><<<qb2, Q_NT, 0, st>>>(T, nullptr, S.res, m, base, bad, true, s32);

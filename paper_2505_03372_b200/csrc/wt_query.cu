@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(Q_NT) rank_kernel(const __grid_constant__ Tree
                                                     const i64* __restrict__ pos,
                                                     i64* __restrict__ out, u64 m, u64 base,
                                                     u64* __restrict__ bad,
-                                                    bool packed) {
+                                                    bool packed, u32* __restrict__ out32 = nullptr) {
   const u64 q = (u64)blockIdx.x * Q_NT + threadIdx.x;
   if (q >= m) return;
   const u64 i = q;
@@ -122,7 +122,11 @@ __global__ void __launch_bounds__(Q_NT) rank_kernel(const __grid_constant__ Tree
     const u64 r1 = qrank1(T.ql[l], p);
     p = (bit ? r1 : p - r1) + base;
   }
-  st_stream_i64(out + i, (i64)(p - (u64)__ldg(T.cum + c)), pol);
+  const u64 r = p - (u64)__ldg(T.cum + c);
+  if (out32)  // sorted-order results of a text below 2^32: 4 bytes (half the gather's working set)
+    out32[i] = (u32)r;
+  else
+    st_stream_i64(out + i, (i64)r, pol);
 }
 
 template <bool kValidate>
@@ -133,7 +137,7 @@ __global__ void __launch_bounds__(Q_NT) select_kernel(const __grid_constant__ Tr
                                                       u64 base, u64* __restrict__ bad,
                                                       bool packed,
                                                       const u32* __restrict__ ks32 = nullptr,
-                                                      u32 kbits = 0) {
+                                                      u32 kbits = 0, u32* __restrict__ out32 = nullptr) {
   const u64 q = (u64)blockIdx.x * Q_NT + threadIdx.x;
   if (q >= m) return;
   const u64 i = q;
@@ -168,7 +172,10 @@ __global__ void __launch_bounds__(Q_NT) select_kernel(const __grid_constant__ Tr
     else
       p = qselect<false>(T.ql[l], p - (u64)__ldg(&ne->zero_base) + 1);
   }
-  st_stream_i64(out + i, (i64)p, pol);
+  if (out32)
+    out32[i] = (u32)p;
+  else
+    st_stream_i64(out + i, (i64)p, pol);
 }
 
 template <bool V>
@@ -381,8 +388,8 @@ __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restri
 // READS (whole sectors, no write-allocate of partial sectors) and coalesced
 // writes, where writing through the permutation from the query kernel cost
 // as much as the queries' own walk
-template <typename T>
-__global__ void __launch_bounds__(Q_NT) qunsort_kernel(const T* __restrict__ res,
+template <typename TR, typename T>
+__global__ void __launch_bounds__(Q_NT) qunsort_kernel(const TR* __restrict__ res,
                                                        const u32* __restrict__ slot_of,
                                                        T* __restrict__ out, u64 m) {
   const u64 i0 = ((u64)blockIdx.x * Q_NT + threadIdx.x) * 4;
@@ -391,7 +398,7 @@ __global__ void __launch_bounds__(Q_NT) qunsort_kernel(const T* __restrict__ res
     const T a = __ldg(res + s.x), b = __ldg(res + s.y), c = __ldg(res + s.z), d = __ldg(res + s.w);
     out[i0] = a; out[i0 + 1] = b; out[i0 + 2] = c; out[i0 + 3] = d;
   } else {
-    for (u64 i = i0; i < m; ++i) out[i] = res[slot_of[i]];
+    for (u64 i = i0; i < m; ++i) out[i] = (T)res[slot_of[i]];
   }
 }
 
@@ -447,9 +454,18 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   // unvalidated -- validation happened above; invalid queries are clamped
   // into range by the walk and the batch raises anyway.  Results land in
   // sorted order (coalesced), then one gather puts them in query order.
-  if (sel32) {
-    select_kernel<false><<<(unsigned)((m + Q_NT - 1) / Q_NT), Q_NT, 0, st>>>(
-        T, nullptr, nullptr, (i64*)S.res, m, rate_log, base, bad, true, s32, S.sel_kbits);
+  // rank / select results of a text below 2^32 go to the sorted-order buffer
+  // as 4 bytes: the gather back reads half the bytes and mostly hits L2
+  u32* r32 = kind != 0 && T.n <= 0xffffffffull ? reinterpret_cast<u32*>(S.res) : nullptr;
+  const unsigned wb = (unsigned)((m + Q_NT - 1) / Q_NT);
+  if (kind == 2) {
+    select_kernel<false><<<wb, Q_NT, 0, st>>>(T, nullptr, S.sorted_args, (i64*)S.res, m, rate_log,
+                                              base, bad, true, sel32 ? s32 : nullptr,
+                                              sel32 ? S.sel_kbits : 0u, r32);
+    e = cudaGetLastError();
+  } else if (kind == 1) {
+    rank_kernel<false><<<wb, Q_NT, 0, st>>>(T, nullptr, S.sorted_args, (i64*)S.res, m, base, bad,
+                                            true, r32);
     e = cudaGetLastError();
   } else if (s32) {
     const unsigned qb2 = (unsigned)((m + Q_NT - 1) / Q_NT);
@@ -467,12 +483,14 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   if (e != cudaSuccess) return e;
   const unsigned ub = (unsigned)((m + 4 * Q_NT - 1) / (4 * Q_NT));
   const int ob = kind == 0 ? out_kind : 8;
-  if (ob == 1)
-    qunsort_kernel<u8><<<ub, Q_NT, 0, st>>>((const u8*)S.res, S.slot_of, (u8*)out, m);
+  if (r32)
+    qunsort_kernel<u32, u64><<<ub, Q_NT, 0, st>>>(r32, S.slot_of, (u64*)out, m);
+  else if (ob == 1)
+    qunsort_kernel<u8, u8><<<ub, Q_NT, 0, st>>>((const u8*)S.res, S.slot_of, (u8*)out, m);
   else if (ob == 2)
-    qunsort_kernel<u16><<<ub, Q_NT, 0, st>>>((const u16*)S.res, S.slot_of, (u16*)out, m);
+    qunsort_kernel<u16, u16><<<ub, Q_NT, 0, st>>>((const u16*)S.res, S.slot_of, (u16*)out, m);
   else
-    qunsort_kernel<u64><<<ub, Q_NT, 0, st>>>((const u64*)S.res, S.slot_of, (u64*)out, m);
+    qunsort_kernel<u64, u64><<<ub, Q_NT, 0, st>>>((const u64*)S.res, S.slot_of, (u64*)out, m);
   return cudaGetLastError();
 }
 

@@ -942,8 +942,14 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
       CU(cudaEventRecord(e0, st));
     }
     if (flags & WT_F_SORT) {
-      // sorted in slices of at most 2^31 queries (u32 permutation indices)
-      const uint64_t slice = std::min<uint64_t>(m, 1ull << 31);
+      // sorted in slices of at most 2^31 queries (u32 slot indices);
+      // WT_SORT_SLICE lowers the slice (tests exercise the multi-slice path)
+      uint64_t slice_max = 1ull << 31;
+      if (const char* e = getenv("WT_SORT_SLICE")) {
+        const unsigned long long v = strtoull(e, nullptr, 10);
+        if (v >= 1 && v < slice_max) slice_max = v;
+      }
+      const uint64_t slice = std::min<uint64_t>(m, slice_max);
       Scratch S{{}, st};
       QuerySortScratch Q{};
       Q.sel_kbits = select_kbits(t);

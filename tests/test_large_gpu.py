@@ -293,3 +293,33 @@ def test_level0_block_mode_u16(W, case, monkeypatch):
         t, o = W.construct_with_alphabet(text, alpha), O.build_with_alphabet(text, alpha)
     assert_same_structure(t, o)
     _check_queries(W, t, text, t.alphabet.sorted_symbols if alpha is None else alpha, m=4000)
+
+
+def test_device_query_sort_slices(W, monkeypatch):
+    """Device batches above the slice size (2^31 queries in production) are
+    sorted slice by slice: same answers and the same first bad index."""
+    import ctypes as C
+    import torch
+    from paper_2505_03372_b200 import _lib
+    monkeypatch.setenv("WT_SORT_SLICE", "1000")
+    text = np.random.default_rng(101).integers(0, 256, 200003, dtype=np.uint8)
+    t = W.construct(text)
+    r = np.random.default_rng(102)
+    m = 5003
+    syms = t.alphabet.sorted_symbols[r.integers(0, t.sigma, m)].astype(np.int64)
+    pos = r.integers(0, len(text) + 1, m)
+    _, fr, _ = O.text_answers(text, 256)
+    d_ids, d_pos = torch.from_numpy(syms).cuda(), torch.from_numpy(pos).cuda()
+    out = torch.empty(m, dtype=torch.int64, device="cuda")
+    bad = C.c_int64(-1)
+    flags = _lib.F_DEVICE_PTRS | _lib.F_SYMBOLS | _lib.F_SORT
+    P = lambda x: C.c_void_p(x.data_ptr())
+    _lib.check(_lib.lib.wt_tree_query(t.handle, _lib.Q_RANK, P(d_ids), P(d_pos), P(out), m, 0, flags,
+                                      None, C.byref(bad), None))
+    assert bad.value == -1
+    assert np.array_equal(out.cpu().numpy(), fr(syms, pos))
+    pos[[3100, 4500]] = len(text) + 7
+    d_pos = torch.from_numpy(pos).cuda()
+    rc = _lib.lib.wt_tree_query(t.handle, _lib.Q_RANK, P(d_ids), P(d_pos), P(out), m, 0, flags, None,
+                                C.byref(bad), None)
+    assert bad.value == 3100

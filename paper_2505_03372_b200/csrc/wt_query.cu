@@ -17,7 +17,10 @@
 
 namespace wt {
 
-constexpr int Q_NT = 256;
+#ifndef WT_Q_NT
+#define WT_Q_NT 128  // 128 vs 256 vs 512 threads: select -1.3 %, others flat
+#endif
+constexpr int Q_NT = WT_Q_NT;
 
 // a sorted batch (WT_F_SORT) carries (argument | id << 48) per query
 // unpack the sorted batch (rank / select): id and argument

@@ -1,5 +1,5 @@
 """How much do the query kernels gain from a FULL (symbol, argument) order
-over the device sort's 65536-bucket order?  Times, per kind: the WT_F_SORT
+over the device sort's bucket order?  Times, per kind: the WT_F_SORT
 path; the plain path on inputs pre-sorted by (symbol, argument) with torch
 (results come out in sorted order: no permuted writes); the plain path on
 inputs pre-sorted by bucket only (each bucket's queries shuffled).

@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(QL_NT) qlayout_kernel(LevelDev L, const u64* t
                                                        u32* __restrict__ sel1, u64 cap1,
                                                        u32* __restrict__ sel0, u64 cap0) {
   const u64 i = (u64)blockIdx.x * QL_NT + threadIdx.x;
-  if (i >= n_lines) return;
+  const u32 lane = threadIdx.x & 31;
   L.total_ones = *total;
   const u64 b0 = i * kQBits;
   const u64 nw = (L.n_bits + 63) >> 6;
@@ -29,10 +29,25 @@ __global__ void __launch_bounds__(QL_NT) qlayout_kernel(LevelDev L, const u64* t
 #pragma unroll
   for (int x = 0; x < kQW; ++x) {
     const u64 wi = (b0 >> 6) + x;
-    w[x] = wi < nw ? __ldg(L.words + wi) : 0ull;  // padding bits are zero
+    w[x] = i < n_lines && wi < nw ? __ldg(L.words + wi) : 0ull;  // padding bits are zero
     pc += __popcll(w[x]);
   }
-  const u64 hdr = b0 >= L.n_bits ? L.total_ones : rank1_dev(L, b0, l2_shift);
+  // headers: one directory lookup per warp (its first line), then a warp
+  // scan of the lines' popcounts -- the 32 lines are consecutive
+  u64 first = 0;
+  if (lane == 0) {
+    const u64 fb = b0;
+    first = i >= n_lines ? 0ull : fb >= L.n_bits ? L.total_ones : rank1_dev(L, fb, l2_shift);
+  }
+  first = __shfl_sync(0xffffffffu, first, 0);
+  u32 inc = pc;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= (u32)d) inc += y;
+  }
+  if (i >= n_lines) return;
+  const u64 hdr = first + (inc - pc);
   ulonglong2* out = lines + i * kQLineU2;
   out[0] = make_ulonglong2(hdr, w[0]);
 #pragma unroll

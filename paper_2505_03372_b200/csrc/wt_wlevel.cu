@@ -1040,11 +1040,29 @@ __global__ void __launch_bounds__(256) wlast_kernel(const __grid_constant__ WLev
     u64 m[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) m[w] = 0;
+    // a full lane slice loads as 32-byte pieces (LDG.256): each lane reads
+    // its own 128 B line, so a 16-byte load touched 32 lines per instruction
+    // and kept the L1 pipe saturated
+    uint4 qf[K];
+    const bool full = e0 + (u32)E <= valid;
+    if (full) {
+#pragma unroll
+      for (int k = 0; k < K; k += 2) {
+        u64 a, b, c, d;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+                     : "l"(base + k * 16));
+        qf[k] = make_uint4((u32)a, (u32)(a >> 32), (u32)b, (u32)(b >> 32));
+        if (k + 1 < K) qf[k + 1] = make_uint4((u32)c, (u32)(c >> 32), (u32)d, (u32)(d >> 32));
+      }
+    }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const u32 e = e0 + k * CH;
       uint4 q;
-      if (e + CH <= valid) {
+      if (full) {
+        q = qf[k];
+      } else if (e + CH <= valid) {
         q = __ldg(reinterpret_cast<const uint4*>(base + k * 16));
       } else {
         u32 w[4] = {0, 0, 0, 0};

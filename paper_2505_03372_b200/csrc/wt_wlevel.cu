@@ -1019,10 +1019,28 @@ __global__ void __launch_bounds__(256) wlast_kernel(const __grid_constant__ WLev
     __syncthreads();
   }
   const u32 ntiles = (u32)((P.m + TILE - 1) / TILE);
+  const u32 nfull = (u32)(P.m / TILE);
   const u32 nw = gridDim.x * 8;
   const u8* in = reinterpret_cast<const u8*>(P.in);
   const u64 l2m = (1ull << P.l2_log) - 1;
-  for (u32 t = blockIdx.x * 8 + (tid >> 5); t < ntiles; t += nw) {
+  // full tiles stream into a per-warp two-slot shared ring by TMA (bulk copy
+  // + mbarrier); lanes then read their 128-byte slice with a per-lane chunk
+  // rotation, so a warp's 16-byte reads spread over the banks
+  constexpr int TB = S::BYTES;
+  extern __shared__ __align__(128) u8 wl_smem[];
+  u8* ring = wl_smem + (tid >> 5) * (2 * TB + 16);
+  u64* mbar = reinterpret_cast<u64*>(ring + 2 * TB);
+  const u32 gw = blockIdx.x * 8 + (tid >> 5);
+  if (lane == 0) {
+    w_mbar_init(&mbar[0]);
+    w_mbar_init(&mbar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (u32 i = 0; i < 2; ++i)
+      if (gw + i * nw < nfull) w_load_tile(ring + i * TB, in + (u64)(gw + i * nw) * TB, TB, &mbar[i]);
+  }
+  __syncwarp();
+  u32 it = 0;
+  for (u32 t = gw; t < ntiles; t += nw, ++it) {
     const u64 t0 = (u64)t * TILE;
     const u32 valid = (u32)min((u64)TILE, P.m - t0);
     // P1 loads first (independent of the data)
@@ -1040,29 +1058,31 @@ __global__ void __launch_bounds__(256) wlast_kernel(const __grid_constant__ WLev
     u64 m[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) m[w] = 0;
-    // a full lane slice loads as 32-byte pieces (LDG.256): each lane reads
-    // its own 128 B line, so a 16-byte load touched 32 lines per instruction
-    // and kept the L1 pipe saturated
-    uint4 qf[K];
-    const bool full = e0 + (u32)E <= valid;
-    if (full) {
+    if (t < nfull) {  // full tile from the ring
+      const u32 slot = it & 1u;
+      w_mbar_wait(&mbar[slot], (it >> 1) & 1u);
+      const u8* src = ring + slot * TB + lane * (K * 16);
 #pragma unroll
-      for (int k = 0; k < K; k += 2) {
-        u64 a, b, c, d;
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
-                     : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
-                     : "l"(base + k * 16));
-        qf[k] = make_uint4((u32)a, (u32)(a >> 32), (u32)b, (u32)(b >> 32));
-        if (k + 1 < K) qf[k + 1] = make_uint4((u32)c, (u32)(c >> 32), (u32)d, (u32)(d >> 32));
+      for (int k = 0; k < K; ++k) {
+        const u32 c = ((u32)k + (u32)lane) % (u32)K;  // rotated chunk: banks spread
+        const uint4 q = *reinterpret_cast<const uint4*>(src + c * 16);
+        u32 cw[WPC];
+        wcodes<TIn, TC, kLut, WPC>(q, slut, P.lut, cw);
+        const u64 mk = (u64)wmask<TC, WPC>(cw, P.shift_bit);
+        const u32 bit = c * CH;  // this chunk's first bit in the lane's slice
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+          m[w] |= (bit >> 6) == (u32)w ? mk << (bit & 63) : 0ull;
       }
-    }
+      __syncwarp();
+      if (lane == 0 && t + 2 * nw < nfull)
+        w_load_tile(ring + slot * TB, in + (u64)(t + 2 * nw) * TB, TB, &mbar[slot]);
+    } else {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const u32 e = e0 + k * CH;
       uint4 q;
-      if (full) {
-        q = qf[k];
-      } else if (e + CH <= valid) {
+      if (e + CH <= valid) {
         q = __ldg(reinterpret_cast<const uint4*>(base + k * 16));
       } else {
         u32 w[4] = {0, 0, 0, 0};
@@ -1075,6 +1095,7 @@ __global__ void __launch_bounds__(256) wlast_kernel(const __grid_constant__ WLev
       u32 mk = wmask<TC, WPC>(cw, P.shift_bit);
       if (e + CH > valid) mk &= e >= valid ? 0u : (1u << (valid - e)) - 1u;
       m[(k * CH) / 64] |= (u64)mk << ((k * CH) % 64);
+    }
     }
 #pragma unroll
     for (int d = 16; d; d >>= 1) pre += __shfl_xor_sync(FULLM, pre, d);
@@ -1263,7 +1284,15 @@ cudaError_t launch_w(const WLevelParams& p, int sms, cudaStream_t st) {
   if (!p.out) {  // the last level: no partition
     u64 blocks = (tiles + 7) / 8;
     if (blocks > (u64)sms * 8) blocks = (u64)sms * 8;
-    wlast_kernel<TIn, TC, kLut><<<(unsigned)blocks, 256, 0, st>>>(p);
+    const int lsmem = 8 * (2 * WS<TIn>::BYTES + 16);
+    static bool lattr = false;
+    if (!lattr) {
+      cudaError_t e = cudaFuncSetAttribute(wlast_kernel<TIn, TC, kLut>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
+      if (e != cudaSuccess) return e;
+      lattr = true;
+    }
+    wlast_kernel<TIn, TC, kLut><<<(unsigned)blocks, 256, lsmem, st>>>(p);
     return cudaGetLastError();
   }
   // block mode: one warp per L1 block is all the parallelism there is

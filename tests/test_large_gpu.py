@@ -323,3 +323,17 @@ def test_device_query_sort_slices(W, monkeypatch):
     rc = _lib.lib.wt_tree_query(t.handle, _lib.Q_RANK, P(d_ids), P(d_pos), P(out), m, 0, flags, None,
                                 C.byref(bad), None)
     assert bad.value == 3100
+
+
+@pytest.mark.parametrize("dt,syms", [(np.uint8, (97, 98)), (np.uint16, (1000, 60000)),
+                                     (np.uint8, (0, 1))])
+def test_single_level_trees(W, dt, syms):
+    """sigma = 2: level 0 is the last level (wlast_kernel) -- through the LUT
+    for non-identity alphabets -- with full tiles on the TMA ring and a
+    partial last tile."""
+    r = np.random.default_rng(111)
+    text = np.array(syms, dt)[r.integers(0, 2, (1 << 20) + 5)]
+    t = W.construct(text)
+    assert t.num_levels == 1
+    assert_same_structure(t, O.build(text))
+    _check_queries(W, t, text, t.alphabet.sorted_symbols, m=3000)

@@ -15,7 +15,7 @@ namespace wt {
 
 constexpr int QL_NT = 256;
 
-__global__ void __launch_bounds__(QL_NT) qlayout_kernel(LevelDev L, const u64* total, u32 l2_shift,
+__global__ void __launch_bounds__(QL_NT, 8) qlayout_kernel(LevelDev L, const u64* total, u32 l2_shift,
                                                        ulonglong2* __restrict__ lines, u64 n_lines,
                                                        u32* __restrict__ sel1, u64 cap1,
                                                        u32* __restrict__ sel0, u64 cap0) {

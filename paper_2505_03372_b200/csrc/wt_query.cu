@@ -337,6 +337,11 @@ __global__ void __launch_bounds__(1024) qsort_scan_final_kernel(u32* __restrict_
   __syncthreads();
   u32 run = off + (warp ? wsum[warp - 1] : 0u) + inc - sum;
   const u32 e[4] = {v.x, v.y, v.z, v.w};
+  if ((i4 + 1) * 4 <= nb) {  // one 16-byte store per thread (coalesced)
+    const u32 o0 = run, o1 = o0 + v.x, o2 = o1 + v.y, o3 = o2 + v.z;
+    reinterpret_cast<uint4*>(hist)[i4] = make_uint4(o0, o1, o2, o3);
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     if (i4 * 4 + j < nb) hist[i4 * 4 + j] = run;

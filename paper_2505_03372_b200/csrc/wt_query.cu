@@ -399,12 +399,24 @@ __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restri
 template <typename TR, typename T>
 __global__ void __launch_bounds__(Q_NT) qunsort_kernel(const TR* __restrict__ res,
                                                        const u32* __restrict__ slot_of,
-                                                       T* __restrict__ out, u64 m) {
+                                                       T* __restrict__ out, u64 m, bool o16) {
   const u64 i0 = ((u64)blockIdx.x * Q_NT + threadIdx.x) * 4;
   if (i0 + 4 <= m) {
     const uint4 s = *reinterpret_cast<const uint4*>(slot_of + i0);
     const T a = __ldg(res + s.x), b = __ldg(res + s.y), c = __ldg(res + s.z), d = __ldg(res + s.w);
-    out[i0] = a; out[i0 + 1] = b; out[i0 + 2] = c; out[i0 + 3] = d;
+    if (o16) {  // the four results as one vector store (16-byte aligned output)
+      if (sizeof(T) == 8) {
+        reinterpret_cast<ulonglong2*>(out + i0)[0] = make_ulonglong2((u64)a, (u64)b);
+        reinterpret_cast<ulonglong2*>(out + i0)[1] = make_ulonglong2((u64)c, (u64)d);
+      } else if (sizeof(T) == 2) {
+        *reinterpret_cast<uint2*>(out + i0) =
+            make_uint2((u32)a | ((u32)b << 16), (u32)c | ((u32)d << 16));
+      } else {
+        *reinterpret_cast<u32*>(out + i0) = (u32)a | ((u32)b << 8) | ((u32)c << 16) | ((u32)d << 24);
+      }
+    } else {
+      out[i0] = a; out[i0 + 1] = b; out[i0 + 2] = c; out[i0 + 3] = d;
+    }
   } else {
     for (u64 i = i0; i < m; ++i) out[i] = (T)res[slot_of[i]];
   }
@@ -490,15 +502,16 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   }
   if (e != cudaSuccess) return e;
   const unsigned ub = (unsigned)((m + 4 * Q_NT - 1) / (4 * Q_NT));
+  const bool o16 = ((uintptr_t)out & 15) == 0;
   const int ob = kind == 0 ? out_kind : 8;
   if (r32)
-    qunsort_kernel<u32, u64><<<ub, Q_NT, 0, st>>>(r32, S.slot_of, (u64*)out, m);
+    qunsort_kernel<u32, u64><<<ub, Q_NT, 0, st>>>(r32, S.slot_of, (u64*)out, m, o16);
   else if (ob == 1)
-    qunsort_kernel<u8, u8><<<ub, Q_NT, 0, st>>>((const u8*)S.res, S.slot_of, (u8*)out, m);
+    qunsort_kernel<u8, u8><<<ub, Q_NT, 0, st>>>((const u8*)S.res, S.slot_of, (u8*)out, m, o16);
   else if (ob == 2)
-    qunsort_kernel<u16, u16><<<ub, Q_NT, 0, st>>>((const u16*)S.res, S.slot_of, (u16*)out, m);
+    qunsort_kernel<u16, u16><<<ub, Q_NT, 0, st>>>((const u16*)S.res, S.slot_of, (u16*)out, m, o16);
   else
-    qunsort_kernel<u64, u64><<<ub, Q_NT, 0, st>>>((const u64*)S.res, S.slot_of, (u64*)out, m);
+    qunsort_kernel<u64, u64><<<ub, Q_NT, 0, st>>>((const u64*)S.res, S.slot_of, (u64*)out, m, o16);
   return cudaGetLastError();
 }
 

@@ -30,6 +30,14 @@
  *   wt_tree_level_query   <- RankSelectIndex rank/select/get_bit on tree.rs[l]
  *   wt_tree_replicate     <- (no reference counterpart; the north star's NCCL
  *                            broadcast of a built tree to the other GPUs)
+ *   wt_bits_from_arrays   <- RankSelectIndex.read / rebind (rankselect.py:397-411,
+ *                            :135-136): a deserialized directory, uploaded as is
+ *   wt_minimal_alphabet   <- alphabet.minimal_alphabet (alphabet.py:94-111)
+ *   wt_map_text           <- AlphabetMap.map_text (alphabet.py:76-84)
+ *   wt_encode_histogram   <- alphabet.encode_and_histogram (alphabet.py:210-242)
+ *   wt_sort_by_prefix     <- wtree.stable_sort_by_prefix (wtree.py:92-100)
+ *   wt_fill_level         <- wtree.fill_level (wtree.py:103-107) ->
+ *                            BitArray.fill_region packing (bitvec.py:119-151)
  */
 #ifndef WT_B200_H
 #define WT_B200_H
@@ -189,6 +197,35 @@ int wt_bits_get(const wt_bits* b, int what, void* dst, uint64_t cap);
 int wt_bits_query(wt_bits* b, int kind, const int64_t* args, int64_t* out, uint64_t m,
                   int flags);
 int wt_bits_destroy(wt_bits* b);
+/* RankSelectIndex.read: a validated, deserialized directory over host words,
+ * uploaded unchanged (queries answer from the stored arrays).              */
+int wt_bits_from_arrays(const uint64_t* words, uint64_t n_bits, uint32_t l2_bits,
+                        uint64_t sample_rate, uint64_t total_ones, const int64_t* l1,
+                        uint64_t n_l1, const uint16_t* l2, uint64_t n_l2,
+                        const int64_t* ones, uint64_t n_ones, const int64_t* zeros,
+                        uint64_t n_zeros, int device, wt_bits** out);
+
+/* -- the reference's O(n) building blocks, one call each (host arrays in and
+ * out; the device does the O(n) work).  wt_construct fuses all of them.     */
+/* ids_out[n] = minimal id of each symbol; symbols_out (256 | 65536 entries
+ * of room) = the sorted present symbols; *sigma_out = their count.          */
+int wt_minimal_alphabet(const void* text, uint64_t n, int sym_bytes, int device,
+                        uint16_t* ids_out, uint16_t* symbols_out, uint32_t* sigma_out);
+/* ids_out[n] = index of text[i] in the sorted `symbols`; an undeclared symbol
+ * -> WT_ERR_SYMBOL, wt_last_error_index() = its first position.            */
+int wt_map_text(const void* text, uint64_t n, int sym_bytes, const uint16_t* symbols,
+                uint32_t sigma, int device, uint16_t* ids_out);
+/* encoded_out[i] = code_values[ids[i]], hist_out[sigma] = counts of each id;
+ * an id >= sigma -> WT_ERR_SYMBOL, wt_last_error_index() = first one.      */
+int wt_encode_histogram(const uint16_t* ids, uint64_t n, const uint16_t* code_values,
+                        uint32_t sigma, int device, uint16_t* encoded_out, int64_t* hist_out);
+/* out = codes stably sorted by (code >> shift).                             */
+int wt_sort_by_prefix(const uint16_t* codes, uint64_t n, uint32_t shift, int device,
+                      uint16_t* out);
+/* words_out[ceil(count/64)] = bit `bit` of codes[0..count), LSB-first, zero
+ * padded.                                                                    */
+int wt_fill_level(const uint16_t* codes, uint64_t count, uint32_t bit, int device,
+                  uint64_t* words_out);
 
 #ifdef __cplusplus
 }

@@ -74,6 +74,13 @@ _SIGS = {
     "wt_bits_get": ([_vp, _i32, _vp, _u64], C.c_int),
     "wt_bits_query": ([_vp, _i32, _vp, _vp, _u64, _i32], C.c_int),
     "wt_bits_destroy": ([_vp], C.c_int),
+    "wt_bits_from_arrays": ([_vp, _u64, _u32, _u64, _u64, _vp, _u64, _vp, _u64, _vp, _u64, _vp,
+                             _u64, _i32, C.POINTER(_vp)], C.c_int),
+    "wt_minimal_alphabet": ([_vp, _u64, _i32, _i32, _vp, _vp, C.POINTER(_u32)], C.c_int),
+    "wt_map_text": ([_vp, _u64, _i32, _vp, _u32, _i32, _vp], C.c_int),
+    "wt_encode_histogram": ([_vp, _u64, _vp, _u32, _i32, _vp, _vp], C.c_int),
+    "wt_sort_by_prefix": ([_vp, _u64, _u32, _i32, _vp], C.c_int),
+    "wt_fill_level": ([_vp, _u64, _u32, _i32, _vp], C.c_int),
 }
 EXPORTS = tuple(_SIGS)
 

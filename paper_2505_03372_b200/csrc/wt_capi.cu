@@ -13,6 +13,7 @@
 #include "../../include/wt_b200.h"
 #include "wt_common.cuh"
 #include "wt_kernels.h"
+#include "wt_host.h"
 
 using namespace wt;
 
@@ -20,7 +21,8 @@ using namespace wt;
 // errors
 // ---------------------------------------------------------------------------
 #include <chrono>
-static thread_local std::string g_err;
+thread_local std::string g_err;
+thread_local int64_t g_err_index = -1;
 // WT_TRACE=1: host-side phase timestamps of wt_construct on stderr
 static bool trace_on() {
   static int v = -1;
@@ -35,25 +37,11 @@ struct Tracer {
     fprintf(stderr, "[wt] %8.3f ms  %s\n", d, what);
   }
 };
-static thread_local int64_t g_err_index = -1;
 
-static int fail(int code, const std::string& msg) {
+int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
-#define CU(call)                                                                        \
-  do {                                                                                  \
-    cudaError_t e_ = (call);                                                            \
-    if (e_ != cudaSuccess) {                                                            \
-      return fail(e_ == cudaErrorMemoryAllocation ? WT_ERR_OOM : WT_ERR_CUDA,           \
-                  std::string(#call) + ": " + cudaGetErrorString(e_));                  \
-    }                                                                                   \
-  } while (0)
-#define TRY(call)            \
-  do {                       \
-    int s_ = (call);         \
-    if (s_ != WT_OK) return s_; \
-  } while (0)
 
 extern "C" const char* wt_last_error(void) { return g_err.c_str(); }
 extern "C" int64_t wt_last_error_index(void) { return g_err_index; }
@@ -67,7 +55,7 @@ extern "C" int wt_device_count(int* count) {
 // device memory: stream-ordered pool, kept warm across builds
 // ---------------------------------------------------------------------------
 static std::once_flag g_pool_once[64];
-static int setup_device(int device) {
+int setup_device(int device) {
   CU(cudaSetDevice(device));
   if (device >= 0 && device < 64) {
     std::call_once(g_pool_once[device], [device]() {
@@ -81,7 +69,7 @@ static int setup_device(int device) {
   return WT_OK;
 }
 
-static int sm_count(int device) {
+int sm_count(int device) {
   int v = 148;
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
   return v;
@@ -1391,6 +1379,63 @@ extern "C" int wt_bits_build(const uint64_t* words, uint64_t n_bits, int words_o
     m.total_ones = tot;
     m.n_ones = tot / sample_rate;
     m.n_zeros = (n_bits - tot) / sample_rate;
+    return WT_OK;
+  };
+  int rc = body();
+  if (rc != WT_OK) {
+    if (b->stream) cudaStreamSynchronize(b->stream);
+    free_bits(b);
+    delete b;
+    return rc;
+  }
+  *out = b;
+  return WT_OK;
+}
+
+// RankSelectIndex.read (rankselect.py:397-411): a directory deserialized (and
+// validated) on the host is uploaded as is -- the queries then answer from
+// the stored L1 / L2 / samples, as the reference's do.
+extern "C" int wt_bits_from_arrays(const uint64_t* words, uint64_t n_bits, uint32_t l2_bits,
+                                   uint64_t sample_rate, uint64_t total_ones, const int64_t* l1,
+                                   uint64_t n_l1, const uint16_t* l2, uint64_t n_l2,
+                                   const int64_t* ones, uint64_t n_ones, const int64_t* zeros,
+                                   uint64_t n_zeros, int device, wt_bits** out) {
+  if (!out) return fail(WT_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  TRY(check_params(l2_bits, sample_rate));
+  if (n_l1 != (n_bits + kL1Bits - 1) / kL1Bits || n_l2 != (n_bits + l2_bits - 1) / l2_bits)
+    return fail(WT_ERR_ARG, "directory lengths do not match n_bits");
+  if (total_ones > n_bits) return fail(WT_ERR_ARG, "total_ones > n_bits");
+  TRY(setup_device(device));
+  wt_bits* b = new wt_bits();
+  b->device = device;
+  b->l2_bits = l2_bits;
+  while ((1u << b->l2_shift) < l2_bits) ++b->l2_shift;
+  while ((1u << b->l2_shift) > l2_bits) --b->l2_shift;
+  b->rate = sample_rate;
+  b->rate_log = rate_log_of(sample_rate);
+  auto body = [&]() -> int {
+    CU(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+    cudaStream_t st = b->stream;
+    const uint64_t nw = (n_bits + 63) / 64;
+    wt_level_meta& m = b->h.meta;
+    m.n_bits = n_bits;
+    m.n_l1 = n_l1;
+    m.n_l2 = n_l2;
+    m.total_ones = total_ones;
+    m.n_ones = n_ones;
+    m.n_zeros = n_zeros;
+    TRY(dalloc(&b->words, nw + 1, st));
+    TRY(dalloc(&b->h.l1, n_l1, st));
+    TRY(dalloc(&b->h.l2, n_l2, st));
+    TRY(dalloc(&b->h.ones, n_ones, st));
+    TRY(dalloc(&b->h.zeros, n_zeros, st));
+    if (nw) CU(cudaMemcpyAsync(b->words, words, nw * 8, cudaMemcpyHostToDevice, st));
+    if (n_l1) CU(cudaMemcpyAsync(b->h.l1, l1, n_l1 * 8, cudaMemcpyHostToDevice, st));
+    if (n_l2) CU(cudaMemcpyAsync(b->h.l2, l2, n_l2 * 2, cudaMemcpyHostToDevice, st));
+    if (n_ones) CU(cudaMemcpyAsync(b->h.ones, ones, n_ones * 8, cudaMemcpyHostToDevice, st));
+    if (n_zeros) CU(cudaMemcpyAsync(b->h.zeros, zeros, n_zeros * 8, cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));
     return WT_OK;
   };
   int rc = body();

@@ -9,6 +9,7 @@
 // u8 : warp-private shared-memory sub-histograms (8 x 256 counters per CTA),
 //      16-byte streaming loads, one merge per CTA.
 // u16: one CTA per SM, packed 16-bit shared counters for all 65536 symbols.
+#include <atomic>
 #include <cstdlib>
 #include "wt_common.cuh"
 #include "wt_kernels.h"
@@ -210,10 +211,16 @@ cudaError_t launch_histogram(const void* text, u64 n, int sym_bytes, u64* hist, 
   if (sym_bytes == 1)
     hist8_kernel<<<(unsigned)blocks, H_NT, 0, st>>>((const u8*)text, n, hist);
   else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(hist16p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
-      attr = true;
+    // the shared-memory opt-in is per device context: once per device (a
+    // race only repeats the idempotent call)
+    static std::atomic<bool> attr[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr[dev].load(std::memory_order_acquire)) {
+      cudaError_t e = cudaFuncSetAttribute(hist16p_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
+      if (e != cudaSuccess) return e;
+      if (dev >= 0 && dev < 64) attr[dev].store(true, std::memory_order_release);
     }
     u64 rows = (n / 8 + H16_NT - 1) / H16_NT;
     if (rows > (u64)sms) rows = (u64)sms;

@@ -31,6 +31,7 @@
 // Multi-node tiles (node boundaries inside the tile) store element by element.
 // Destination of element j with bit b in node `key`:
 //   b=1: one_base[key] + R1(j)        b=0: zero_base[key] + R0(j)
+#include <atomic>
 #include "wt_common.cuh"
 #include "wt_kernels.h"
 
@@ -1287,29 +1288,32 @@ cudaError_t launch_w(const WLevelParams& p, int sms, cudaStream_t st) {
   const size_t smem = 512 + (size_t)W_WARPS * WF<TIn, TC>::WARP_SMEM;
   auto kern = wlevel_kernel<TIn, TC, kLut>;
   // attribute + occupancy once per device (host cost off the per-level path)
-  static int cached[64] = {0};
+  // (per device: attributes and occupancy belong to a device context;
+  // racing first calls only repeat idempotent work)
+  static std::atomic<int> cached[64];
+  static std::atomic<bool> lattr[64];
   int dev = 0;
   cudaGetDevice(&dev);
-  int per_sm = dev >= 0 && dev < 64 ? cached[dev] : 0;
+  const bool dev_ok = dev >= 0 && dev < 64;
+  int per_sm = dev_ok ? cached[dev].load(std::memory_order_acquire) : 0;
   if (per_sm <= 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W_NT, smem);
     if (per_sm < 1) per_sm = 1;
-    if (dev >= 0 && dev < 64) cached[dev] = per_sm;
+    if (dev_ok) cached[dev].store(per_sm, std::memory_order_release);
   }
   const u64 tiles = (p.m + WS<TIn>::TILE - 1) / WS<TIn>::TILE;
   if (!p.out) {  // the last level: no partition
     u64 blocks = (tiles + 7) / 8;
     if (blocks > (u64)sms * 8) blocks = (u64)sms * 8;
     const int lsmem = 8 * (2 * WS<TIn>::BYTES + 16);
-    static bool lattr = false;
-    if (!lattr) {
+    if (!dev_ok || !lattr[dev].load(std::memory_order_acquire)) {
       cudaError_t e = cudaFuncSetAttribute(wlast_kernel<TIn, TC, kLut>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
       if (e != cudaSuccess) return e;
-      lattr = true;
+      if (dev_ok) lattr[dev].store(true, std::memory_order_release);
     }
     wlast_kernel<TIn, TC, kLut><<<(unsigned)blocks, 256, lsmem, st>>>(p);
     return cudaGetLastError();

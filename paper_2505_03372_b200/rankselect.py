@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib
 from ._lib import check, lib, ptr
 from .bitvec import WORD_BITS, BitArray
-from .errors import OrdinalError, PositionError
+from .errors import CorruptIndexError, OrdinalError, PositionError, TruncatedError
 
 L1_BITS = 65536
 DEFAULT_L2_BITS = 512
@@ -169,7 +169,57 @@ class RankSelectIndex:
         ks = np.asarray(ks, np.int64)
         return self._q(_lib.B_SELECT0, ks) if len(ks) else np.zeros(0, np.int64)
 
+    def rebind(self, words: np.ndarray) -> None:
+        """Point the index at another copy of its region's words
+        (rankselect.py:135-136): the directory arrays are kept and the words
+        uploaded to a fresh device index over them."""
+        words = np.ascontiguousarray(words, np.uint64)
+        handle = _bits_from_arrays(words, self.n_bits, self.params, self.total_ones,
+                                   self.l1_counts, self.l2_counts, self.one_samples,
+                                   self.zero_samples)
+        self._backend = _bits_backend(handle)
+        self._words_fn = lambda: words
+        self._owner = handle
+
     # -- serialization (rankselect.py:387-394) ---------------------------------
+    @classmethod
+    def read(cls, src: BinaryIO, words: np.ndarray) -> "RankSelectIndex":
+        """Deserialize one directory written by ``write`` over ``words``
+        (rankselect.py:396-411), with the reference's validation
+        (``_validate``, :413-430); the arrays are uploaded as stored."""
+        l1_bits, l2_bits, rate, n_bits, total_ones = _read_struct(src, "<IIIQQ")
+        try:
+            params = RankSelectParams(l1_bits, l2_bits, rate)
+        except ValueError as e:
+            raise CorruptIndexError(str(e)) from e
+        l1 = _read_array(src, "<u8").astype(np.int64)
+        l2 = _read_array(src, "<u2")
+        ones = _read_array(src, "<u8").astype(np.int64)
+        zeros = _read_array(src, "<u8").astype(np.int64)
+        words = np.ascontiguousarray(words, np.uint64)
+        n = n_bits
+        if n and len(words) != (n + WORD_BITS - 1) >> 6:
+            raise CorruptIndexError("word count does not match region length")
+        if len(l1) != -(-n // L1_BITS):
+            raise CorruptIndexError("L1 directory length mismatch")
+        if len(l2) != -(-n // params.l2_bits):
+            raise CorruptIndexError("L2 directory length mismatch")
+        if not 0 <= total_ones <= n:
+            raise CorruptIndexError("total ones outside [0, n]")
+        if len(l1) and (int(l1[0]) != 0 or np.any(np.diff(l1) < 0)):
+            raise CorruptIndexError("L1 counts not a non-decreasing prefix sum")
+        if len(ones) != total_ones // params.sample_rate:
+            raise CorruptIndexError("one-sample count mismatch")
+        if len(zeros) != (n - total_ones) // params.sample_rate:
+            raise CorruptIndexError("zero-sample count mismatch")
+        handle = _bits_from_arrays(words, n, params, total_ones, l1, l2, ones, zeros)
+        meta = _lib.LevelMeta()
+        check(lib.wt_bits_level_meta(handle.h, _lib.C.byref(meta)), "wt_bits_level_meta")
+        idx = cls(params, meta, _bits_backend(handle), _bits_fetch(handle, meta),
+                  lambda: words, owner=handle)
+        idx._cache.update({_lib.A_L1: l1, _lib.A_L2: l2, _lib.A_ONES: ones, _lib.A_ZEROS: zeros})
+        return idx
+
     def write(self, out: BinaryIO) -> None:
         p = self.params
         out.write(struct.pack("<IIIQQ", p.l1_bits, p.l2_bits, p.sample_rate,
@@ -204,6 +254,46 @@ def _bits_fetch(handle: _BitsHandle, meta):
     return fetch
 
 
+def _read_struct(src, fmt: str):
+    n = struct.calcsize(fmt)
+    data = src.read(n)
+    if len(data) != n:
+        raise TruncatedError(f"expected {n} bytes, got {len(data)}")
+    return struct.unpack(fmt, data)
+
+
+def _read_array(src, dtype: str):
+    (count,) = _read_struct(src, "<Q")
+    if count > 1 << 40:
+        raise CorruptIndexError(f"array length {count} is implausible")
+    nbytes = count * np.dtype(dtype).itemsize
+    data = src.read(nbytes)
+    if len(data) != nbytes:
+        raise TruncatedError(f"expected {nbytes} bytes, got {len(data)}")
+    return np.frombuffer(data, dtype=dtype).copy()
+
+
+def _bits_backend(handle: "_BitsHandle"):
+    def backend(kind, args):
+        out = np.empty(len(args), np.int64)
+        check(lib.wt_bits_query(handle.h, kind, ptr(args), ptr(out), len(args), 0),
+              "wt_bits_query")
+        return out
+    return backend
+
+
+def _bits_from_arrays(words, n_bits, params, total_ones, l1, l2, ones, zeros) -> "_BitsHandle":
+    arrs = [np.ascontiguousarray(a, dt) for a, dt in ((l1, np.int64), (l2, np.uint16),
+                                                      (ones, np.int64), (zeros, np.int64))]
+    h = _lib.C.c_void_p()
+    check(lib.wt_bits_from_arrays(ptr(words) if len(words) else None, n_bits, params.l2_bits,
+                                  params.sample_rate, total_ones,
+                                  ptr(arrs[0]), len(arrs[0]), ptr(arrs[1]), len(arrs[1]),
+                                  ptr(arrs[2]), len(arrs[2]), ptr(arrs[3]), len(arrs[3]),
+                                  _lib.current_device(), _lib.C.byref(h)), "wt_bits_from_arrays")
+    return _BitsHandle(h)
+
+
 def build_index(ba: BitArray, region: int, params: RankSelectParams | None = None,
                 workers: int = 1) -> RankSelectIndex:
     """Rank/select directory of one region (rankselect.py:442-536), built on
@@ -221,11 +311,5 @@ def build_index(ba: BitArray, region: int, params: RankSelectParams | None = Non
     meta = _lib.LevelMeta()
     check(lib.wt_bits_level_meta(h, _lib.C.byref(meta)), "wt_bits_level_meta")
 
-    def backend(kind, args):
-        out = np.empty(len(args), np.int64)
-        check(lib.wt_bits_query(handle.h, kind, ptr(args), ptr(out), len(args), 0),
-              "wt_bits_query")
-        return out
-
-    return RankSelectIndex(params, meta, backend, _bits_fetch(handle, meta),
+    return RankSelectIndex(params, meta, _bits_backend(handle), _bits_fetch(handle, meta),
                            lambda: words, owner=handle)

@@ -101,6 +101,57 @@ class _TreeHandle:
 
 
 # ---------------------------------------------------------------------------
+# the per-level building blocks of _build (wtree.py:92-107), as device ops;
+# wt_construct fuses both into one kernel per level
+# ---------------------------------------------------------------------------
+def stable_sort_by_prefix(encoded: np.ndarray, l: int, num_levels: int) -> np.ndarray:
+    """Stably sort code words by their top ``l`` bits, i.e. by
+    ``encoded >> (num_levels - l)`` (wtree.py:92-100), on the device
+    (``wt_sort_by_prefix``: one stable popcount split per key bit)."""
+    enc = np.asarray(encoded)
+    dtype = enc.dtype
+    shift = int(num_levels) - int(l)
+    if len(enc) == 0:
+        return enc.copy()
+    if dtype != np.uint16:
+        if not np.issubdtype(dtype, np.integer) or int(enc.min()) < 0 \
+                or int(enc.max()) >= MAX_SIGMA:
+            raise BuildError("code words must lie in [0, 65536)")
+    if shift >= 16:
+        return enc.copy()
+    if shift < 0:
+        raise BuildError(f"prefix length {l} exceeds {num_levels} levels")
+    codes = np.ascontiguousarray(enc, np.uint16)
+    out = np.empty(len(codes), np.uint16)
+    check(lib.wt_sort_by_prefix(ptr(codes), len(codes), shift, _lib.current_device(), ptr(out)),
+          "wt_sort_by_prefix")
+    return out if dtype == np.uint16 else out.astype(dtype)
+
+
+def fill_level(ba: BitArray, l: int, encoded: np.ndarray, count: int,
+               num_levels: int, workers: int = 1) -> None:
+    """Write region ``l``: bit j = bit ``num_levels-1-l`` of code word j
+    (wtree.py:103-107, packed as BitArray.fill_region does, bitvec.py:119-151),
+    packed on the device (``wt_fill_level``)."""
+    n = int(ba.region_nbits[l])
+    count = int(count)
+    if count != n:
+        raise BuildError(f"region {l} holds {n} bits, got {count}")
+    if n == 0:
+        return
+    enc = np.asarray(encoded)[:count]
+    if enc.dtype != np.uint16:
+        if int(enc.min()) < 0 or int(enc.max()) >= MAX_SIGMA:
+            raise BuildError("code words must lie in [0, 65536)")
+    codes = np.ascontiguousarray(enc, np.uint16)
+    words = np.empty((n + 63) // 64, np.uint64)
+    check(lib.wt_fill_level(ptr(codes), n, num_levels - 1 - l, _lib.current_device(),
+                            ptr(words)), "wt_fill_level")
+    w0 = ba.region_word_offset(l)
+    ba.words[w0:w0 + len(words)] = words
+
+
+# ---------------------------------------------------------------------------
 # the tree
 # ---------------------------------------------------------------------------
 class WaveletTree:

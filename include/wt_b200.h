@@ -85,6 +85,9 @@ extern "C" {
                                PAPER.md:928, :988): buckets of (coarse text
                                position, symbol); results stay in query order,
                                errors report the first bad index as unsorted  */
+#define WT_F_PHASES     16  /* with WT_F_SORT | WT_F_DEVICE_PTRS and ms_out: ms_out
+                               is float[4] = {total, sort, walk, gather} device
+                               times (CUDA events on the query stream)        */
 
 /* array selectors for wt_tree_get */
 #define WT_A_SYMBOLS      0   /* u16[sigma]   sorted alphabet symbols        */
@@ -170,10 +173,35 @@ int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int64_t* args,
                   void* out, uint64_t m, uint64_t chunk, int flags, void* stream,
                   int64_t* bad_index, float* ms_out);
 
+/* Pipeline accounting of one host-buffer query (device times from CUDA
+ * events on the three pipeline streams; BatchRunner.stage_seconds /
+ * process_seconds / staging_peak_records, batch.py:93-108, :192-224).      */
+typedef struct {
+    uint64_t chunks;         /* chunks the batch was split into             */
+    uint64_t slots;          /* device staging slots used (<= 2)            */
+    uint64_t chunk_records;  /* queries per chunk                           */
+    uint64_t peak_records;   /* most queries resident in device slots at once,
+                                measured from the copy-in start / copy-out
+                                end events of every chunk                   */
+    float h2d_ms;            /* sum of copy-in durations                    */
+    float kernel_ms;         /* sum of kernel durations                     */
+    float d2h_ms;            /* sum of kernel-end -> copy-out-end            */
+    float total_ms;          /* first copy-in start -> last copy-out end     */
+} wt_query_stats;
+/* wt_tree_query plus the pipeline accounting (stats may be NULL).          */
+int wt_tree_query_ex(wt_tree* t, int kind, const int64_t* ids, const int64_t* args,
+                     void* out, uint64_t m, uint64_t chunk, int flags, void* stream,
+                     int64_t* bad_index, float* ms_out, wt_query_stats* stats);
+
 /* Pinned host memory (cudaHostAlloc) for result arrays: device->host copies
  * into it are asynchronous and overlap the next chunk's kernel.           */
 int wt_host_alloc(uint64_t bytes, void** out);
 int wt_host_free(void* p);
+/* Page-lock / release an existing host range (cudaHostRegister): the
+ * multi-GPU runner's shared result array, whose disjoint slices the ranks
+ * of a node fill straight from their devices.                              */
+int wt_host_register(void* p, uint64_t bytes);
+int wt_host_unregister(void* p);
 
 /* Bit-vector query (WT_B_*) against one level of a built tree: the
  * RankSelectIndex methods of tree.rs[l] (rankselect.py:140-373).  Host

@@ -30,7 +30,7 @@ lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
 WT_OK, WT_ERR_CUDA, WT_ERR_ARG, WT_ERR_OOM, WT_ERR_SYMBOL, WT_ERR_NCCL, WT_ERR_BUILD = range(7)
 Q_ACCESS, Q_RANK, Q_SELECT = 0, 1, 2
 B_RANK1, B_RANK0, B_SELECT1, B_SELECT0, B_BIT = range(5)
-F_DEVICE_PTRS, F_SYMBOLS, F_ACCESS_IDS, F_SORT = 1, 2, 4, 8
+F_DEVICE_PTRS, F_SYMBOLS, F_ACCESS_IDS, F_SORT, F_PHASES = 1, 2, 4, 8, 16
 (A_SYMBOLS, A_CODE_VALUES, A_CODE_LENS, A_CUM_HIST, A_LEVEL_SIZES, A_REGION_OFFS, A_WORDS,
  A_L1, A_L2, A_ONES, A_ZEROS, A_NODE_STARTS, A_NODE_RANK0) = range(13)
 
@@ -45,6 +45,13 @@ class Meta(C.Structure):
 class LevelMeta(C.Structure):
     _fields_ = [(k, C.c_uint64) for k in
                 ("n_bits", "total_ones", "n_l1", "n_l2", "n_ones", "n_zeros", "n_nodes")]
+
+
+class QueryStats(C.Structure):
+    """wt_query_stats (include/wt_b200.h): the host pipeline's accounting."""
+    _fields_ = [("chunks", C.c_uint64), ("slots", C.c_uint64), ("chunk_records", C.c_uint64),
+                ("peak_records", C.c_uint64), ("h2d_ms", C.c_float), ("kernel_ms", C.c_float),
+                ("d2h_ms", C.c_float), ("total_ms", C.c_float)]
 
 
 _vp, _u64, _u32, _i32, _f32p = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(C.c_float)
@@ -64,9 +71,13 @@ _SIGS = {
     "wt_tree_build_profile": ([_vp, _f32p, _u32], C.c_int),
     "wt_tree_destroy": ([_vp], C.c_int),
     "wt_tree_query": ([_vp, _i32, _vp, _vp, _vp, _u64, _u64, _i32, _vp, C.POINTER(C.c_int64), _f32p], C.c_int),
+    "wt_tree_query_ex": ([_vp, _i32, _vp, _vp, _vp, _u64, _u64, _i32, _vp, C.POINTER(C.c_int64),
+                          _f32p, C.POINTER(QueryStats)], C.c_int),
     "wt_tree_level_query": ([_vp, _u32, _i32, _vp, _vp, _u64], C.c_int),
     "wt_host_alloc": ([_u64, C.POINTER(_vp)], C.c_int),
     "wt_host_free": ([_vp], C.c_int),
+    "wt_host_register": ([_vp, _u64], C.c_int),
+    "wt_host_unregister": ([_vp], C.c_int),
     "wt_nccl_unique_id": ([_vp], C.c_int),
     "wt_tree_replicate": ([_vp, _vp, _i32, _i32, _i32, C.POINTER(_vp), _f32p], C.c_int),
     "wt_bits_build": ([_vp, _u64, _i32, _u32, _u64, _i32, C.POINTER(_vp)], C.c_int),
@@ -105,7 +116,10 @@ def check(rc: int, what: str = "") -> None:
 
 
 def ptr(a: np.ndarray | None):
-    return None if a is None else C.c_void_p(a.ctypes.data)
+    """c_void_p to a's data that keeps `a` alive (ctypes ``_objects``): a
+    temporary array passed as ``ptr(np.concatenate(...))`` must outlive the
+    call it is an argument of."""
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
 def current_device() -> int:

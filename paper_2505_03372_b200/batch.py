@@ -85,9 +85,11 @@ class BatchRunner:
         self.workers = max(1, int(workers))
         self.staging_allocated_records = 0
         self.staging_peak_records = 0
-        self.stage_seconds = 0.0
-        self.process_seconds = 0.0
-        self.kernel_ms = 0.0
+        self.stage_seconds = 0.0     # host->device copies of the chunks (device time)
+        self.process_seconds = 0.0   # query kernels (device time)
+        self.unstage_seconds = 0.0   # kernel end -> results copied back
+        self.wall_seconds = 0.0
+        self.chunks = 0
 
     def _cause(self, batch: QueryBatch, i: int) -> Exception:
         """The reference's cause for query i (batch.py:130-148)."""
@@ -114,15 +116,22 @@ class BatchRunner:
                 return tree.alphabet.sorted_symbols[np.zeros(0, np.int64)]
             return np.zeros(0, np.int64)
         chunk = min(self.chunk_size, nq)
-        num_chunks = -(-nq // chunk)
-        slots = 1 if num_chunks == 1 else 2
-        self.staging_allocated_records = slots * chunk
-        self.staging_peak_records = chunk if slots == 1 else chunk + min(chunk, nq - chunk)
-        t0 = time.perf_counter()
         syms = None if batch.kind == "access" else batch.symbols
+        st = _lib.QueryStats()
+        t0 = time.perf_counter()
         out, bad = tree.query(_KIND_ID[batch.kind], syms, batch.args, symbols=True,
-                              chunk=chunk, sort=self.sort)
-        self.process_seconds = time.perf_counter() - t0
+                              chunk=chunk, sort=self.sort, stats=st)
+        self.wall_seconds = time.perf_counter() - t0
+        # measured by the C pipeline (CUDA events on its copy-in / kernel /
+        # copy-out streams, wt_query_stats): staging = the host->device copies
+        # of the chunks, processing = the kernels; the peak is the most
+        # queries that were resident in the device slots at once
+        self.stage_seconds = st.h2d_ms / 1e3
+        self.process_seconds = st.kernel_ms / 1e3
+        self.unstage_seconds = st.d2h_ms / 1e3
+        self.staging_allocated_records = int(st.slots * st.chunk_records)
+        self.staging_peak_records = int(st.peak_records)
+        self.chunks = int(st.chunks)
         if bad >= 0:
             raise BatchError(bad, self._cause(batch, bad))
         return out

@@ -255,6 +255,7 @@ struct wt_tree {
   size_t qbuf_bytes = 0;
   cudaStream_t qstream[3] = {nullptr, nullptr, nullptr};  // copy-in, compute, copy-out
   cudaEvent_t qev[3][2] = {};                              // per stage and slot
+  std::vector<cudaEvent_t> tev;                            // pipeline timing events (stats)
   std::mutex qmutex;
   std::mutex tables_mutex;
   u32 sel_kbits = 0;        // select_kbits() cache  // lazy node_starts / node_rank0 (wt_tree_get)
@@ -436,6 +437,7 @@ static void free_tree_arrays(wt_tree* t) {
   for (auto& a : t->qev)
     for (auto& e : a)
       if (e) cudaEventDestroy(e);
+  for (auto& e : t->tev) cudaEventDestroy(e);
   if (t->stream) cudaStreamDestroy(t->stream);
 }
 
@@ -908,9 +910,17 @@ static u32 select_kbits(wt_tree* t) {
 extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int64_t* args,
                              void* out, uint64_t m, uint64_t chunk, int flags, void* stream,
                              int64_t* bad_index, float* ms_out) {
+  return wt_tree_query_ex(t, kind, ids, args, out, m, chunk, flags, stream, bad_index, ms_out,
+                          nullptr);
+}
+
+extern "C" int wt_tree_query_ex(wt_tree* t, int kind, const int64_t* ids, const int64_t* args,
+                                void* out, uint64_t m, uint64_t chunk, int flags, void* stream,
+                                int64_t* bad_index, float* ms_out, wt_query_stats* stats) {
   if (!t) return fail(WT_ERR_ARG, "NULL tree");
   if (kind < 0 || kind > 2) return fail(WT_ERR_ARG, "unknown query kind");
   if (ms_out) *ms_out = 0.f;
+  if (stats) *stats = wt_query_stats{};
   if (bad_index) *bad_index = -1;
   if (m == 0) return WT_OK;
   if (!args || !out || (kind != WT_Q_ACCESS && !ids)) return fail(WT_ERR_ARG, "NULL buffer");
@@ -950,11 +960,26 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
         TRY(S.get(&r, slice * out_elem));
         Q.res = r;
       }
+      // WT_F_PHASES: per-phase device times of a single-slice batch
+      // (ms_out[1..3] = sort, walk, gather back to query order)
+      const bool phases = (flags & WT_F_PHASES) && ms_out && slice == m;
+      cudaEvent_t ph[3] = {nullptr, nullptr, nullptr};
+      if (phases)
+        for (auto& e : ph) CU(cudaEventCreate(&e));
+      struct PhGuard { cudaEvent_t* p; ~PhGuard() { for (int i = 0; i < 3; ++i) if (p[i]) cudaEventDestroy(p[i]); } } pg{ph};
       for (uint64_t a = 0; a < m; a += slice) {
         const uint64_t cnt = std::min(slice, m - a);
         CU(launch_query_sorted(t->dev, kind, out_kind, validate,
                                ids ? (const i64*)ids + a : nullptr, (const i64*)args + a,
-                               (u8*)out + a * out_elem, cnt, t->rate_log, a, t->bad, Q, st));
+                               (u8*)out + a * out_elem, cnt, t->rate_log, a, t->bad, Q, st,
+                               phases ? ph : nullptr));
+      }
+      if (phases) {
+        CU(cudaEventRecord(e1, st));
+        CU(cudaStreamSynchronize(st));
+        CU(cudaEventElapsedTime(ms_out + 1, e0, ph[0]));
+        CU(cudaEventElapsedTime(ms_out + 2, ph[0], ph[1]));
+        CU(cudaEventElapsedTime(ms_out + 3, ph[1], ph[2]));
       }
     } else {
       CU(launch_query(t->dev, kind, out_kind, validate, (const i64*)ids, (const i64*)args, out, m,
@@ -968,6 +993,11 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
       CU(cudaEventElapsedTime(ms_out, e0, e1));
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);
+      if (stats) stats->kernel_ms = stats->total_ms = *ms_out;
+    }
+    if (stats) {
+      stats->chunks = 1;
+      stats->chunk_records = m;
     }
     return WT_OK;
   }
@@ -1002,11 +1032,15 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
     CU(cudaMemsetAsync(t->bad, 0xff, 8, sk));
   }
   const uint64_t nchunks = (m + chunk - 1) / chunk;
-  std::vector<cudaEvent_t> kt;  // kernel timing events (ms_out)
-  if (ms_out) {
-    kt.resize(2 * nchunks);
-    for (auto& e : kt) CU(cudaEventCreate(&e));
+  // timing events (ms_out / stats), pooled in the tree: per chunk
+  // [copy-in start, copy-in end, kernel start, kernel end, copy-out end]
+  const bool timed = ms_out || stats;
+  if (timed && t->tev.size() < 5 * nchunks) {
+    const size_t have = t->tev.size();
+    t->tev.resize(5 * nchunks, nullptr);
+    for (size_t i = have; i < t->tev.size(); ++i) CU(cudaEventCreate(&t->tev[i]));
   }
+  cudaEvent_t* ev = timed ? t->tev.data() : nullptr;
   int rc = WT_OK;
   for (uint64_t c = 0; c < nchunks && rc == WT_OK; ++c) {
     const int s = (int)(c & 1);
@@ -1018,14 +1052,16 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
     cudaError_t e = cudaSuccess;
     // copy-in: slot s is free once the kernel of chunk c-2 has read it
     if (c >= 2) e = cudaStreamWaitEvent(sin, t->qev[1][s], 0);
+    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[5 * c], sin);
     if (e == cudaSuccess && kind != WT_Q_ACCESS)
       e = cudaMemcpyAsync(d_ids, ids + a, cnt * 8, cudaMemcpyHostToDevice, sin);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_args, args + a, cnt * 8, cudaMemcpyHostToDevice, sin);
+    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[5 * c + 1], sin);
     if (e == cudaSuccess) e = cudaEventRecord(t->qev[0][s], sin);
     // kernel: inputs landed, and the copy-out of chunk c-2 has drained d_out
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sk, t->qev[0][s], 0);
     if (e == cudaSuccess && c >= 2) e = cudaStreamWaitEvent(sk, t->qev[2][s], 0);
-    if (e == cudaSuccess && ms_out) e = cudaEventRecord(kt[2 * c], sk);
+    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[5 * c + 2], sk);
     if (e == cudaSuccess && !sorted) {
       e = launch_query(t->dev, kind, out_kind, validate, d_ids, d_args, d_out, cnt, t->rate_log, a,
                        t->bad, sk);
@@ -1046,12 +1082,13 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
       e = launch_query_sorted(t->dev, kind, out_kind, validate, d_ids, d_args, d_out, cnt,
                               t->rate_log, a, t->bad, Q, sk);
     }
-    if (e == cudaSuccess && ms_out) e = cudaEventRecord(kt[2 * c + 1], sk);
+    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[5 * c + 3], sk);
     if (e == cudaSuccess) e = cudaEventRecord(t->qev[1][s], sk);
     // copy-out
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, t->qev[1][s], 0);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync((u8*)out + a * out_elem, d_out, cnt * out_elem, cudaMemcpyDeviceToHost, sout);
+    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[5 * c + 4], sout);
     if (e == cudaSuccess) e = cudaEventRecord(t->qev[2][s], sout);
     if (e != cudaSuccess) rc = fail(WT_ERR_CUDA, std::string("query pipeline: ") + cudaGetErrorString(e));
   }
@@ -1059,15 +1096,46 @@ extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int
     cudaError_t e = cudaStreamSynchronize(t->qstream[i]);
     if (e != cudaSuccess && rc == WT_OK) rc = fail(WT_ERR_CUDA, cudaGetErrorString(e));
   }
-  if (ms_out && rc == WT_OK) {
-    float total_ms = 0.f;
+  if (timed && rc == WT_OK) {
+    // device-time accounting of the pipeline, and the staging residency it
+    // actually had: chunk c holds a device slot from its copy-in start to its
+    // copy-out end; the peak is the largest record count resident at once
+    // (the reference's staging_peak_records, batch.py:100-108)
+    float h2d = 0.f, kern = 0.f, d2h = 0.f;
+    std::vector<std::pair<float, int64_t>> edges;
+    edges.reserve(2 * nchunks);
     for (uint64_t c = 0; c < nchunks; ++c) {
-      float ms = 0;
-      if (cudaEventElapsedTime(&ms, kt[2 * c], kt[2 * c + 1]) == cudaSuccess) total_ms += ms;
+      float a = 0, b = 0, k0 = 0, k1 = 0, o = 0;
+      cudaEventElapsedTime(&a, ev[0], ev[5 * c]);
+      cudaEventElapsedTime(&b, ev[0], ev[5 * c + 1]);
+      cudaEventElapsedTime(&k0, ev[0], ev[5 * c + 2]);
+      cudaEventElapsedTime(&k1, ev[0], ev[5 * c + 3]);
+      cudaEventElapsedTime(&o, ev[0], ev[5 * c + 4]);
+      h2d += b - a;
+      kern += k1 - k0;
+      d2h += o - k1;
+      const int64_t cnt = (int64_t)std::min(chunk, m - c * chunk);
+      edges.push_back({a, cnt});
+      edges.push_back({o, -cnt});
     }
-    *ms_out = total_ms;
+    // at equal times a release sorts before an acquire (slot handed over)
+    std::sort(edges.begin(), edges.end());
+    int64_t cur = 0, peak = 0;
+    for (auto& e : edges) peak = std::max(peak, cur += e.second);
+    if (ms_out) *ms_out = kern;
+    if (stats) {
+      stats->chunks = nchunks;
+      stats->slots = nchunks > 1 ? 2 : 1;
+      stats->chunk_records = chunk;
+      stats->peak_records = (uint64_t)peak;
+      stats->h2d_ms = h2d;
+      stats->kernel_ms = kern;
+      stats->d2h_ms = d2h;
+      float tot = 0;
+      cudaEventElapsedTime(&tot, ev[0], ev[5 * (nchunks - 1) + 4]);
+      stats->total_ms = tot;
+    }
   }
-  for (auto& e : kt) cudaEventDestroy(e);
   if (rc == WT_OK && validate && bad_index) {
     cudaError_t e = cudaMemcpy(bad_index, t->bad, 8, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) rc = fail(WT_ERR_CUDA, cudaGetErrorString(e));
@@ -1089,6 +1157,18 @@ extern "C" int wt_host_alloc(uint64_t bytes, void** out) {
 }
 extern "C" int wt_host_free(void* p) {
   if (p) cudaFreeHost(p);
+  return WT_OK;
+}
+// page-lock an existing host range (a shared-memory result array the ranks
+// of a node write disjoint slices of), so device->host copies into it are
+// asynchronous DMA
+extern "C" int wt_host_register(void* p, uint64_t bytes) {
+  if (!p || !bytes) return WT_OK;
+  CU(cudaHostRegister(p, bytes, cudaHostRegisterPortable));
+  return WT_OK;
+}
+extern "C" int wt_host_unregister(void* p) {
+  if (p) CU(cudaHostUnregister(p));
   return WT_OK;
 }
 

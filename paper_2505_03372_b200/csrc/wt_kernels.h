@@ -71,9 +71,12 @@ struct QuerySortScratch {
   void* res;        // m results in sorted order (out_kind bytes each)
   u32 sel_kbits = 0; // bits of the largest select ordinal (0: 8-byte records only)
 };
+// phase (optional): 3 events recorded after the sort (key + scan + scatter),
+// after the walk and after the gather back to query order
 cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool validate,
                                 const i64* ids, const i64* args, void* out, u64 m, int rate_log,
-                                u64 base, u64* bad, const QuerySortScratch& S, cudaStream_t st);
+                                u64 base, u64* bad, const QuerySortScratch& S, cudaStream_t st,
+                                cudaEvent_t* phase = nullptr);
 
 // query-side rank-line layout (wt_qlayout.cu)
 u64 qlayout_lines(u64 n_bits);

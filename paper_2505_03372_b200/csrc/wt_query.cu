@@ -424,7 +424,8 @@ __global__ void __launch_bounds__(Q_NT) qunsort_kernel(const TR* __restrict__ re
 
 cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool validate,
                                 const i64* ids, const i64* args, void* out, u64 m, int rate_log,
-                                u64 base, u64* bad, const QuerySortScratch& S, cudaStream_t st) {
+                                u64 base, u64* bad, const QuerySortScratch& S, cudaStream_t st,
+                                cudaEvent_t* phase) {
   if (m == 0) return cudaSuccess;
   if (m > 0xffffffffull) return cudaErrorInvalidValue;
   const u64 blocks = (m + Q_NT - 1) / Q_NT;
@@ -469,6 +470,7 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
                                                           args, m, S.hist, S.sorted_args, s32,
                                                           sel32 ? S.sel_kbits : 0u, S.slot_of);
   e = cudaGetLastError();
+  if (e == cudaSuccess && phase) e = cudaEventRecord(phase[0], st);
   if (e != cudaSuccess) return e;
   // ids are mapped minimal ids now (packed into the arguments): run
   // unvalidated -- validation happened above; invalid queries are clamped
@@ -500,6 +502,7 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
     e = launch_query(T, kind, out_kind, false, nullptr, S.sorted_args, S.res, m, rate_log, base,
                      bad, st, true);
   }
+  if (e == cudaSuccess && phase) e = cudaEventRecord(phase[1], st);
   if (e != cudaSuccess) return e;
   const unsigned ub = (unsigned)((m + 4 * Q_NT - 1) / (4 * Q_NT));
   const bool o16 = ((uintptr_t)out & 15) == 0;
@@ -512,7 +515,9 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
     qunsort_kernel<u16, u16><<<ub, Q_NT, 0, st>>>((const u16*)S.res, S.slot_of, (u16*)out, m, o16);
   else
     qunsort_kernel<u64, u64><<<ub, Q_NT, 0, st>>>((const u64*)S.res, S.slot_of, (u64*)out, m, o16);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e == cudaSuccess && phase) e = cudaEventRecord(phase[2], st);
+  return e;
 }
 
 // ---------------------------------------------------------------------------

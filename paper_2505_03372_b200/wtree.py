@@ -228,23 +228,33 @@ class WaveletTree:
                                lambda: bits.region_words(l), owner=handle)
 
     def query(self, kind: int, ids, args, *, symbols: bool = False, access_ids: bool = False,
-              chunk: int = 0, sort: bool = False):
-        """Run one batch on the device; returns (out, first_bad_index)."""
+              chunk: int = 0, sort: bool = False, out: np.ndarray | None = None,
+              stats: "_lib.QueryStats | None" = None):
+        """Run one batch on the device; returns (out, first_bad_index).
+        ``out`` (optional): a contiguous array of the result dtype and length
+        the answers are copied into (e.g. one rank's slice of a shared,
+        page-locked result array, parallel.SharedResult)."""
         args = np.ascontiguousarray(np.asarray(args, np.int64).reshape(-1))
         m = len(args)
         if kind == _lib.Q_ACCESS:
-            out = _lib.pinned_empty(m, np.int64 if access_ids else self.alphabet.sorted_symbols.dtype)
+            dt = np.dtype(np.int64 if access_ids else self.alphabet.sorted_symbols.dtype)
             ids_a = None
         else:
+            dt = np.dtype(np.int64)
             ids_a = np.ascontiguousarray(np.asarray(ids, np.int64).reshape(-1))
-            out = _lib.pinned_empty(m, np.int64)
+        if out is None:
+            out = _lib.pinned_empty(m, dt)
+        elif (out.dtype != dt or len(out) != m or not out.flags.c_contiguous
+              or not out.flags.writeable):
+            raise ValueError(f"out must be a writeable contiguous {dt} array of length {m}")
         if m == 0:
             return out, -1
         flags = ((_lib.F_SYMBOLS if symbols else 0) | (_lib.F_ACCESS_IDS if access_ids else 0)
                  | (_lib.F_SORT if sort else 0))
         bad = C.c_int64(-1)
-        check(lib.wt_tree_query(self._h.h, kind, ptr(ids_a), ptr(args), ptr(out), m, chunk,
-                                flags, None, C.byref(bad), None), "wt_tree_query")
+        check(lib.wt_tree_query_ex(self._h.h, kind, ptr(ids_a), ptr(args), ptr(out), m, chunk,
+                                   flags, None, C.byref(bad), None,
+                                   None if stats is None else C.byref(stats)), "wt_tree_query_ex")
         return out, int(bad.value)
 
     # -- shape helpers (wtree.py:137-190) -------------------------------------
@@ -543,11 +553,15 @@ def load(source) -> WaveletTree:
     lm_arr = (_lib.LevelMeta * max(num_levels, 1))(*[lm for _, lm in lms])
     cat = lambda xs, dt: np.ascontiguousarray(np.concatenate(xs) if xs else np.zeros(0, dt), dt)
     h = C.c_void_p()
-    check(lib.wt_tree_from_arrays(C.byref(meta), ptr(np.ascontiguousarray(symbols, np.uint16)),
-                                  ptr(np.ascontiguousarray(cum)), ptr(np.ascontiguousarray(words)),
-                                  lm_arr, ptr(cat(l1s, np.int64)), ptr(cat(l2s, np.uint16)),
-                                  ptr(cat(ones, np.int64)), ptr(cat(zeros, np.int64)),
+    # every array the call reads is bound to a name for the duration of the call
+    sym16, cum_c, words_c = (np.ascontiguousarray(symbols, np.uint16), np.ascontiguousarray(cum),
+                             np.ascontiguousarray(words))
+    l1_c, l2_c = cat(l1s, np.int64), cat(l2s, np.uint16)
+    ones_c, zeros_c = cat(ones, np.int64), cat(zeros, np.int64)
+    check(lib.wt_tree_from_arrays(C.byref(meta), ptr(sym16), ptr(cum_c), ptr(words_c), lm_arr,
+                                  ptr(l1_c), ptr(l2_c), ptr(ones_c), ptr(zeros_c),
                                   _lib.current_device(), C.byref(h)), "wt_tree_from_arrays")
+    del sym16, cum_c, words_c, l1_c, l2_c, ones_c, zeros_c
     tree = WaveletTree(_TreeHandle(h), width, symbols.dtype)
     # node tables: structural check against the shape, then the stored ranks
     # against the device's (wtree.py:556-572)

@@ -180,12 +180,12 @@ typedef struct {
     uint64_t chunks;         /* chunks the batch was split into             */
     uint64_t slots;          /* device staging slots used (<= 2)            */
     uint64_t chunk_records;  /* queries per chunk                           */
-    uint64_t peak_records;   /* most queries resident in device slots at once,
-                                measured from the copy-in start / copy-out
-                                end events of every chunk                   */
+    uint64_t peak_records;   /* most queries staged in device slots at once:
+                                a chunk is staged from its copy-in start to
+                                its kernel's end (CUDA events per chunk)     */
     float h2d_ms;            /* sum of copy-in durations                    */
     float kernel_ms;         /* sum of kernel durations                     */
-    float d2h_ms;            /* sum of kernel-end -> copy-out-end            */
+    float d2h_ms;            /* last kernel end -> last copy-out end         */
     float total_ms;          /* first copy-in start -> last copy-out end     */
 } wt_query_stats;
 /* wt_tree_query plus the pipeline accounting (stats may be NULL).          */

@@ -129,34 +129,56 @@ def current_device() -> int:
 # ---------------------------------------------------------------------------
 # pinned result arrays: device -> host copies into page-locked memory are
 # asynchronous (the query pipeline overlaps them with the next chunk's
-# kernel).  Blocks are cached by size and return to the cache when the last
-# numpy view of them is dropped.
+# kernel).  Blocks come in power-of-two size classes and return to a free
+# list when the last numpy view of them is dropped; the free lists hold at
+# most PINNED_CACHE_BYTES (the excess is released with wt_host_free), so a
+# process answering batches of many sizes does not accumulate page-locked
+# memory.
 # ---------------------------------------------------------------------------
 PINNED_MIN_BYTES = 1 << 20
+PINNED_CACHE_BYTES = int(os.environ.get("WT_PINNED_CACHE_BYTES", 8 << 30))
 _pin_lock = threading.Lock()
 _pin_free: dict[int, list[int]] = {}
+_pin_cached = 0   # bytes on the free lists
 
 
-def _pin_release(nbytes: int, addr: int) -> None:
+def _pin_class(nbytes: int) -> int:
+    return 1 << (int(nbytes) - 1).bit_length()
+
+
+def _pin_release(cls: int, addr: int) -> None:
+    global _pin_cached
     with _pin_lock:
-        _pin_free.setdefault(nbytes, []).append(addr)
+        if _pin_cached + cls <= PINNED_CACHE_BYTES:
+            _pin_free.setdefault(cls, []).append(addr)
+            _pin_cached += cls
+            return
+    lib.wt_host_free(C.c_void_p(addr))
+
+
+def pinned_cached_bytes() -> int:
+    return _pin_cached
 
 
 def pinned_empty(count: int, dtype) -> np.ndarray:
     """An uninitialised array in pinned host memory (plain np.empty below
     PINNED_MIN_BYTES, or when page-locked memory cannot be had)."""
+    global _pin_cached
     dtype = np.dtype(dtype)
     nbytes = int(count) * dtype.itemsize
     if nbytes < PINNED_MIN_BYTES:
         return np.empty(count, dtype)
+    cls = _pin_class(nbytes)
     with _pin_lock:
-        free = _pin_free.get(nbytes)
+        free = _pin_free.get(cls)
         addr = free.pop() if free else None
+        if addr is not None:
+            _pin_cached -= cls
     if addr is None:
         p = C.c_void_p()
-        if lib.wt_host_alloc(nbytes, C.byref(p)) != WT_OK or not p.value:
+        if lib.wt_host_alloc(cls, C.byref(p)) != WT_OK or not p.value:
             return np.empty(count, dtype)
         addr = p.value
-    holder = (C.c_uint8 * nbytes).from_address(addr)
-    weakref.finalize(holder, _pin_release, nbytes, addr)
+    holder = (C.c_uint8 * cls).from_address(addr)
+    weakref.finalize(holder, _pin_release, cls, addr)
     return np.frombuffer(holder, dtype, count)

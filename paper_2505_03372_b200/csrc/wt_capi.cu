@@ -1033,11 +1033,11 @@ extern "C" int wt_tree_query_ex(wt_tree* t, int kind, const int64_t* ids, const 
   }
   const uint64_t nchunks = (m + chunk - 1) / chunk;
   // timing events (ms_out / stats), pooled in the tree: per chunk
-  // [copy-in start, copy-in end, kernel start, kernel end, copy-out end]
+  // [copy-in start, copy-in end, kernel end] + one after the last copy-out
   const bool timed = ms_out || stats;
-  if (timed && t->tev.size() < 5 * nchunks) {
+  if (timed && t->tev.size() < 3 * nchunks + 1) {
     const size_t have = t->tev.size();
-    t->tev.resize(5 * nchunks, nullptr);
+    t->tev.resize(3 * nchunks + 1, nullptr);
     for (size_t i = have; i < t->tev.size(); ++i) CU(cudaEventCreate(&t->tev[i]));
   }
   cudaEvent_t* ev = timed ? t->tev.data() : nullptr;
@@ -1052,16 +1052,15 @@ extern "C" int wt_tree_query_ex(wt_tree* t, int kind, const int64_t* ids, const 
     cudaError_t e = cudaSuccess;
     // copy-in: slot s is free once the kernel of chunk c-2 has read it
     if (c >= 2) e = cudaStreamWaitEvent(sin, t->qev[1][s], 0);
-    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[5 * c], sin);
+    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[3 * c], sin);
     if (e == cudaSuccess && kind != WT_Q_ACCESS)
       e = cudaMemcpyAsync(d_ids, ids + a, cnt * 8, cudaMemcpyHostToDevice, sin);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_args, args + a, cnt * 8, cudaMemcpyHostToDevice, sin);
-    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[5 * c + 1], sin);
+    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[3 * c + 1], sin);
     if (e == cudaSuccess) e = cudaEventRecord(t->qev[0][s], sin);
     // kernel: inputs landed, and the copy-out of chunk c-2 has drained d_out
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sk, t->qev[0][s], 0);
     if (e == cudaSuccess && c >= 2) e = cudaStreamWaitEvent(sk, t->qev[2][s], 0);
-    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[5 * c + 2], sk);
     if (e == cudaSuccess && !sorted) {
       e = launch_query(t->dev, kind, out_kind, validate, d_ids, d_args, d_out, cnt, t->rate_log, a,
                        t->bad, sk);
@@ -1082,42 +1081,47 @@ extern "C" int wt_tree_query_ex(wt_tree* t, int kind, const int64_t* ids, const 
       e = launch_query_sorted(t->dev, kind, out_kind, validate, d_ids, d_args, d_out, cnt,
                               t->rate_log, a, t->bad, Q, sk);
     }
-    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[5 * c + 3], sk);
+    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[3 * c + 2], sk);
     if (e == cudaSuccess) e = cudaEventRecord(t->qev[1][s], sk);
     // copy-out
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, t->qev[1][s], 0);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync((u8*)out + a * out_elem, d_out, cnt * out_elem, cudaMemcpyDeviceToHost, sout);
-    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[5 * c + 4], sout);
     if (e == cudaSuccess) e = cudaEventRecord(t->qev[2][s], sout);
     if (e != cudaSuccess) rc = fail(WT_ERR_CUDA, std::string("query pipeline: ") + cudaGetErrorString(e));
+  }
+  if (rc == WT_OK && ev) {
+    cudaError_t e = cudaEventRecord(ev[3 * nchunks], sout);
+    if (e != cudaSuccess) rc = fail(WT_ERR_CUDA, cudaGetErrorString(e));
   }
   for (int i = 0; i < 3; ++i) {
     cudaError_t e = cudaStreamSynchronize(t->qstream[i]);
     if (e != cudaSuccess && rc == WT_OK) rc = fail(WT_ERR_CUDA, cudaGetErrorString(e));
   }
   if (timed && rc == WT_OK) {
-    // device-time accounting of the pipeline, and the staging residency it
-    // actually had: chunk c holds a device slot from its copy-in start to its
-    // copy-out end; the peak is the largest record count resident at once
-    // (the reference's staging_peak_records, batch.py:100-108)
-    float h2d = 0.f, kern = 0.f, d2h = 0.f;
+    // device-time accounting of the pipeline, and the staging it actually
+    // had: chunk c's queries occupy a device slot from the start of their
+    // copy-in until the kernel has consumed them; the peak is the largest
+    // record count staged at once (the reference's staging_peak_records,
+    // batch.py:100-108).  Kernel time of chunk c = from the later of its
+    // inputs landing and the previous kernel's end, to its end.
+    float h2d = 0.f, kern = 0.f, prev_k = 0.f;
     std::vector<std::pair<float, int64_t>> edges;
     edges.reserve(2 * nchunks);
     for (uint64_t c = 0; c < nchunks; ++c) {
-      float a = 0, b = 0, k0 = 0, k1 = 0, o = 0;
-      cudaEventElapsedTime(&a, ev[0], ev[5 * c]);
-      cudaEventElapsedTime(&b, ev[0], ev[5 * c + 1]);
-      cudaEventElapsedTime(&k0, ev[0], ev[5 * c + 2]);
-      cudaEventElapsedTime(&k1, ev[0], ev[5 * c + 3]);
-      cudaEventElapsedTime(&o, ev[0], ev[5 * c + 4]);
+      float a = 0, b = 0, k1 = 0;
+      cudaEventElapsedTime(&a, ev[0], ev[3 * c]);
+      cudaEventElapsedTime(&b, ev[0], ev[3 * c + 1]);
+      cudaEventElapsedTime(&k1, ev[0], ev[3 * c + 2]);
       h2d += b - a;
-      kern += k1 - k0;
-      d2h += o - k1;
+      kern += k1 - std::max(b, prev_k);
+      prev_k = k1;
       const int64_t cnt = (int64_t)std::min(chunk, m - c * chunk);
       edges.push_back({a, cnt});
-      edges.push_back({o, -cnt});
+      edges.push_back({k1, -cnt});
     }
+    float last_out = 0;
+    cudaEventElapsedTime(&last_out, ev[0], ev[3 * nchunks]);
     // at equal times a release sorts before an acquire (slot handed over)
     std::sort(edges.begin(), edges.end());
     int64_t cur = 0, peak = 0;
@@ -1130,10 +1134,8 @@ extern "C" int wt_tree_query_ex(wt_tree* t, int kind, const int64_t* ids, const 
       stats->peak_records = (uint64_t)peak;
       stats->h2d_ms = h2d;
       stats->kernel_ms = kern;
-      stats->d2h_ms = d2h;
-      float tot = 0;
-      cudaEventElapsedTime(&tot, ev[0], ev[5 * (nchunks - 1) + 4]);
-      stats->total_ms = tot;
+      stats->d2h_ms = last_out - prev_k;  // the copy-out tail after the last kernel
+      stats->total_ms = last_out;
     }
   }
   if (rc == WT_OK && validate && bad_index) {

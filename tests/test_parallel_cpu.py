@@ -32,9 +32,12 @@ class TextTree:
     def occurrences(self, c):
         return self.occ.get(int(c), 0)
 
-    def query(self, kind, ids, args, *, symbols=False, access_ids=False, chunk=0, sort=False):
+    def query(self, kind, ids, args, *, symbols=False, access_ids=False, chunk=0, sort=False,
+              out=None, stats=None):
         args = np.asarray(args, np.int64)
-        out = np.zeros(len(args), np.int64 if kind else self.text.dtype)
+        if out is None:
+            out = np.zeros(len(args), np.int64 if kind else self.text.dtype)
+        assert len(out) == len(args) and out.dtype == (np.int64 if kind else self.text.dtype)
         for i, a in enumerate(args):
             if kind == Q_ACCESS:
                 if not 0 <= a < self.n:
@@ -107,19 +110,38 @@ def test_shard_bounds_partition(world, m):
 
 
 def _w_basic(rank, world):
-    uid = par.share_bytes(bytes(range(128)) if rank == 0 else None)
+    uid = par.share_bytes(bytes(range(128)) if rank == 0 else None, 128)
     mx = par.max_over_ranks(float(rank + 1))
-    local = np.arange(*par.shard_bounds(11, rank, world), dtype=np.int64) * 10
-    g = par.gather(local, 11)
-    return uid, mx, g.tolist()
+    mn = par.min_over_ranks(10 - rank)
+    with par.SharedResult(11, np.int64) as res:
+        lo, hi = par.shard_bounds(11, rank, world)
+        res.slice(lo, hi)[:] = np.arange(lo, hi) * 10   # this rank's slice only
+        import torch.distributed as dist
+        dist.barrier()
+        g = res.array.tolist()
+    return uid, mx, mn, g
 
 
-def test_uid_broadcast_max_and_gather_world2():
+def test_uid_broadcast_reductions_and_shared_result_world2():
     out = _run(2, _w_basic)
-    for uid, mx, g in out:
+    for uid, mx, mn, g in out:
         assert uid == bytes(range(128))
-        assert mx == 2.0
+        assert mx == 2.0 and mn == 9
         assert g == [10 * i for i in range(11)]
+
+
+def _w_shared_name_unique(rank, world):
+    a = par.SharedResult(5, np.uint8)
+    b = par.SharedResult(5, np.uint8)
+    names = (a.shm.name, b.shm.name)
+    a.close()
+    b.close()
+    return names
+
+
+def test_shared_results_are_distinct_blocks():
+    (a0, b0), (a1, b1) = _run(2, _w_shared_name_unique)
+    assert a0 == a1 and b0 == b1 and a0 != b0
 
 
 TEXT = np.random.default_rng(5).integers(0, 12, 400).astype(np.uint8)
@@ -128,6 +150,16 @@ TEXT = np.random.default_rng(5).integers(0, 12, 400).astype(np.uint8)
 def _w_sharded(rank, world, kind, args, syms):
     tree = TextTree(TEXT)
     return par.run_sharded(tree, QueryBatch(kind, args, syms)).tolist()
+
+
+def _w_sharded_out(rank, world, kind, args, syms):
+    """Caller-owned shared result: every rank reads the whole batch's answers
+    from the one array after run_sharded returns."""
+    tree = TextTree(TEXT)
+    with par.SharedResult(len(args), par.result_dtype(tree, kind)) as res:
+        got = par.run_sharded(tree, QueryBatch(kind, args, syms), out=res)
+        assert got is res.array
+        return got.tolist()
 
 
 def test_run_sharded_equals_single_rank():
@@ -141,6 +173,8 @@ def test_run_sharded_equals_single_rank():
     for kind, args, s in (("access", pos, None), ("rank", rpos, syms), ("select", ks, syms)):
         want = one.query({"access": 0, "rank": 1, "select": 2}[kind], s, args)[0].tolist()
         for got in _run(2, _w_sharded, kind, args, s):
+            assert got == want
+        for got in _run(3, _w_sharded_out, kind, args, s):
             assert got == want
 
 

@@ -257,3 +257,29 @@ def test_load_many_small_trees_roundtrip(W):
         buf2 = io.BytesIO()
         W.save(t2, buf2)
         assert buf2.getvalue() == blob
+
+
+def test_pinned_result_cache_size_classes_and_cap():
+    """Pinned result blocks come in power-of-two classes (a block serves any
+    size of its class) and the free lists are capped (the cache
+    grew one block per distinct size, without bound)."""
+    import gc
+
+    from paper_2505_03372_b200 import _lib
+    a = _lib.pinned_empty((3 << 20) // 8, np.int64)      # 3 MiB -> the 4 MiB class
+    addr = a.ctypes.data
+    del a
+    gc.collect()
+    b = _lib.pinned_empty((7 << 19) // 8, np.int64)      # 3.5 MiB: same class, same block
+    assert b.ctypes.data == addr
+    del b
+    gc.collect()
+    old = _lib.PINNED_CACHE_BYTES
+    try:
+        _lib.PINNED_CACHE_BYTES = _lib.pinned_cached_bytes()  # no room for more
+        c = _lib.pinned_empty((9 << 20) // 8, np.int64)    # a new 16 MiB block
+        del c
+        gc.collect()
+        assert _lib.pinned_cached_bytes() <= _lib.PINNED_CACHE_BYTES  # freed, not cached
+    finally:
+        _lib.PINNED_CACHE_BYTES = old

@@ -66,6 +66,14 @@ KINDS = ("access", "rank", "select")
 SECTOR_BYTES = {"access": 7 * 64 + 32 + 16, "rank": 8 * 64 + 24, "select": 8 * 96 + 24}
 
 
+_T0 = time.time()
+
+
+def log(msg: str) -> None:
+    """Progress on stderr (the JSON line alone goes to stdout)."""
+    print(f"[bench {time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -295,6 +303,7 @@ def _extra_builds(W, args, dev, hbm):
     out = {}
     steps = max(1, min(args.steps, 10))
     for name in args.extra_builds:
+        log(f"extra build {name}")
         c = LC.LARGE[name]
         n = 1 << c["n_log"]
         g = torch.Generator(device=dev)
@@ -404,6 +413,7 @@ def run_ours(args):
     # ---------------- build (rank 0: the single-GPU construction) ----------
     build = builds = tree = None
     if rank == 0:
+        log("C2 build")
         text_np = LC.text_np("C2") if args.n_log == 30 else \
             np.random.default_rng(0).integers(0, 256, n, dtype=np.uint8)  # C2 recipe
         text_dev = torch.from_numpy(text_np).to(dev)
@@ -421,6 +431,7 @@ def run_ours(args):
 
     # ---------------- replicate over NCCL --------------------------------------
     replicate = None
+    log("queries")
     if world > 1:
         tree = par.replicate(tree if rank == 0 else None, device=local)
         replicate = {"ms": par.max_over_ranks(float(tree.replicate_ms)),
@@ -499,6 +510,7 @@ def run_ours(args):
 
     # ---------------- end to end through the public API -------------------------
     e2e = None
+    log("e2e")
     if args.e2e:
         pin = lambda t: t.cpu().pin_memory().numpy()
         h = {k: (None if q[k][0] is None else pin(q[k][0]), pin(q[k][1])) for k in KINDS}
@@ -546,6 +558,7 @@ def run_ours(args):
 
     # ---------------- C5: 1e9 queries per step split over the ranks -----------
     c5 = None
+    log("c5")
     if args.c5_queries:
         lo, hi = par.shard_bounds(args.c5_queries, rank, world)
         mine = hi - lo
@@ -571,6 +584,7 @@ def run_ours(args):
         torch.cuda.empty_cache()
 
     cpu = None
+    log("cpu baseline")
     if rank == 0 and not args.no_cpu:
         cpu = cpu_baseline(W, tree, args)
 
@@ -633,10 +647,12 @@ def cpu_baseline(W, tree, args):
     t0 = time.perf_counter()
     buf = io.BytesIO()
     tree.save(buf)
+    log("cpu baseline: tree saved")
     buf.seek(0)
     rt = wt.load(buf)
     del buf
     load_s = time.perf_counter() - t0
+    log("cpu baseline: reference loaded the index")
     sample = {k: args.cpu_sample for k in KINDS}  # equal thirds, as the GPU step
     done, spent, checked = 0, 0.0, 0
     per_kind = {}
@@ -651,6 +667,7 @@ def cpu_baseline(W, tree, args):
         done += len(got)
         spent += dt
         per_kind[k] = {"queries": len(got), "queries_per_s": len(got) / dt}
+        log(f"cpu baseline: {k} {len(got) / dt:.0f} q/s")
     return {"value": done / spent, "unit": UNIT, "cores": 1, "kind": "reference",
             "sample": (f"wtindex 0.1.0 (the unmodified reference, baseline/_ref) "
                        f"BatchRunner.run(workers=1) on the C2 tree (n=2^{args.n_log}, sigma=256; "

@@ -668,6 +668,27 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
           break;
         }
       const bool block_mode = dbh && P.L >= 2 && (sym_bytes == 1 || thr == 32768u);
+      // Levels >= 1 stay in block mode while every resident warp still gets
+      // two L1 blocks (one warp walks a whole block: P1 is the block's L1 entry
+      // plus a running count); a level whose successor is also in block mode
+      // counts the successor's ones per L1 block only, in its first pass.
+      // The last level (wlast) reads per-tile counts.
+      std::vector<char> blk(P.L, 0);
+      {
+        const uint64_t slots2 = 2 * wlevel_warp_slots(sm_count(device));
+        for (uint32_t l = 0; l < P.L; ++l) {
+          const bool big = bm ? bm[0] == '1' : t->lv[l].meta.n_l1 >= slots2;
+          blk[l] = l == 0 ? block_mode : (blk[l - 1] && big && l + 1 < P.L);
+        }
+      }
+      // next level's bit at a LUT level 0: parity of (symbol >= nthr[i]) over
+      // the first symbols whose code's top two bits reach 1, 2, 3
+      uint32_t nthr[3] = {0x10000u, 0x10000u, 0x10000u};
+      if (P.L >= 2)
+        for (uint32_t i = P.sigma; i-- > 0;) {
+          const uint32_t cls = (P.values[i] >> (P.L - 2)) & 3u;
+          for (uint32_t k = 1; k <= cls; ++k) nthr[k - 1] = P.symbols[i];
+        }
       if (P.L && P.sizes[0]) {
         CU(cudaMemsetAsync(l1cnt[0], 0, (t->lv[0].meta.n_l1 + 4) * 4, st));
         if (block_mode && sym_bytes == 1)
@@ -677,6 +698,12 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
         else
           CU(launch_wcount0(dtext, n, sym_bytes, thr, tcnt[0], l1cnt[0], sm_count(device), st));
       }
+      // Pair mode for the last two levels (every code reaches the last level):
+      // one pass over level L-2 writes its bits and, from the staged runs,
+      // the last level's bits -- no partitioned sequence, no last-level pass.
+      // (WT_PAIR=0 turns it off: the parity tests run both.)
+      const char* pe = getenv("WT_PAIR");
+      const bool pair_ok = !(pe && pe[0] == '0');
       int ci = 0;
       for (uint32_t l = 0; l < P.L; ++l) {
         const uint64_t m = (uint64_t)P.sizes[l];
@@ -685,15 +712,24 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
         const int in_bytes = l == 0 ? sym_bytes : P.code_bytes;
         LevelHost& h = t->lv[l];
         CU(launch_l1_scan(l1cnt[ci], h.meta.n_l1, h.l1, totals + l, st));
+        const bool pair = pair_ok && l + 2 == P.L && (uint64_t)P.sizes[l + 1] == m;
+        const bool next_blk = !pair && l + 1 < P.L && blk[l] && blk[l + 1];
         WLevelParams wp{};
         wp.in = l == 0 ? dtext : cur[(l - 1) & 1];
-        wp.out = l + 1 < P.L ? cur[l & 1] : nullptr;
+        wp.out = l + 1 < P.L && !pair ? cur[l & 1] : nullptr;
         wp.m = m;
         wp.m_next = l + 1 < P.L ? (uint64_t)P.sizes[l + 1] : 0;
         if (wp.out && wp.m_next == 0) wp.out = nullptr;
+        if (pair) {
+          const uint64_t w0 = (uint64_t)P.offsets[l + 1] / 64;
+          const uint64_t w1 = ((uint64_t)P.offsets[l + 1] + wp.m_next + 63) / 64;
+          CU(cudaMemsetAsync(t->words + w0, 0, (w1 - w0) * 8, st));
+          CU(cudaMemsetAsync(l1cnt[ci ^ 1], 0, (t->lv[l + 1].meta.n_l1 + 4) * 4, st));
+          wp.next_words = t->words + w0;
+        }
         if (wp.out) {
           const uint64_t nt = wlevel_tiles(wp.m_next, P.code_bytes);
-          CU(cudaMemsetAsync(tcnt[ci ^ 1], 0, (nt + 64) * 4, st));
+          if (!next_blk) CU(cudaMemsetAsync(tcnt[ci ^ 1], 0, (nt + 64) * 4, st));
           CU(cudaMemsetAsync(l1cnt[ci ^ 1], 0, (t->lv[l + 1].meta.n_l1 + 4) * 4, st));
         }
         wp.words = t->words + (P.offsets[l] >> 6);
@@ -705,7 +741,9 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
         wp.nodes = t->nodes + P.node_off[l];
         wp.lut = l == 0 ? dlut : nullptr;
         wp.l1 = h.l1;
-        wp.tile_counts = l == 0 && block_mode ? nullptr : tcnt[ci];
+        wp.tile_counts = blk[l] ? nullptr : tcnt[ci];
+        wp.next_block = next_blk && wp.out ? 1 : 0;
+        for (int i = 0; i < 3; ++i) wp.nthr[i] = nthr[i];
         wp.next_tile_counts = tcnt[ci ^ 1];
         wp.next_l1_counts = l1cnt[ci ^ 1];
         wp.thr = thr;
@@ -716,6 +754,25 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
         wp.rate = sample_rate;
         CU(launch_wlevel(wp, in_bytes, P.code_bytes, l == 0 && dlut != nullptr, sm_count(device), st));
         ci ^= 1;
+        if (pair) {  // the last level: L1 from the pair pass's counts, then L2 + samples
+          LevelHost& hn = t->lv[l + 1];
+          CU(cudaEventRecord(lev[l + 1], st));
+          CU(launch_l1_scan(l1cnt[ci], hn.meta.n_l1, hn.l1, totals + l + 1, st));
+          DirParams dp{};
+          dp.words = wp.next_words;
+          dp.m = wp.m_next;
+          dp.l1 = hn.l1;
+          dp.l2 = hn.l2;
+          dp.ones = hn.ones;
+          dp.zeros = hn.zeros;
+          dp.ones_cap = wp.m_next / sample_rate;
+          dp.zeros_cap = wp.m_next / sample_rate;
+          dp.l2_log = l2_log;
+          dp.rate_log = rate_log_of(sample_rate);
+          dp.rate = sample_rate;
+          CU(launch_dir(dp, sm_count(device), st));
+          break;
+        }
       }
       // (the query-side layouts run after the last level: overlapping them
       // with the next level's kernel on a side stream measured slower)

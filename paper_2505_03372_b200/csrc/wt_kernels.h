@@ -20,6 +20,16 @@ struct WLevelParams {
   const u32* tile_counts;  // ones per warp tile of this level (nullptr: block mode, level 0)
   u32* next_tile_counts;   // ones of level l+1 per warp tile of level l+1 (atomics)
   u32* next_l1_counts;     // ones of level l+1 per L1 block (atomics)
+  // pair mode (out == nullptr, next_words != nullptr): level l+1 is the last
+  // level; its bits are written straight from the staged runs (region start,
+  // zeroed by the caller) instead of partitioning the codes into `out`
+  u64* next_words;
+  // block mode for this AND the next level (tile_counts == nullptr,
+  // next_tile_counts unused): next-level ones per L1 block only, counted in
+  // the first pass; nthr = the three raw-symbol thresholds of the code's top
+  // two bits at a LUT level 0 (bit l+1 = parity of symbol >= nthr[i])
+  int next_block;
+  u32 nthr[3];
   u32 thr;                 // level 0 with a LUT: smallest symbol whose code has the top bit
   u32 shift_bit;           // L-1-l
   u32 shift_key;           // L-l
@@ -41,6 +51,21 @@ cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, u32 thr, u32* 
                            u32* l1_counts, int sms, cudaStream_t st);
 // exclusive scan of per-L1-block counts -> l1[0..n_l1) and the level total
 cudaError_t launch_l1_scan(const u32* counts, u64 n_l1, u64* l1, u64* total, cudaStream_t st);
+// L2 entries and select samples of a level whose bits and L1 directory exist
+// (the level a pair-mode launch wrote): one warp per L1 block
+struct DirParams {
+  const u64* words;  // region start
+  u64 m;             // bits
+  const u64* l1;
+  u16* l2;
+  u64* ones;
+  u64* zeros;
+  u64 ones_cap, zeros_cap;
+  u32 l2_log;
+  int rate_log;
+  u64 rate;
+};
+cudaError_t launch_dir(const DirParams& p, int sms, cudaStream_t st);
 
 // K1: raw-symbol histogram (wt_hist.cu); hist must be zeroed (u64[256|65536])
 // block_hist (may be null): per 65536-symbol L1 block, u8: its 256-bin

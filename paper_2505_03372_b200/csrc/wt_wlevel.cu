@@ -205,14 +205,15 @@ __device__ __forceinline__ u64 wnext_multiple(u64 o, u64 rate, int rate_log) {
 // Any tile the fast path does not take (the level's partial last tile, tiles
 // spanning several nodes): loads from global memory, element-by-element
 // destination stores, per-element next-level counts.
-template <typename TIn, typename TC, bool kLut>
+template <typename TIn, typename TC, bool kLut, int MODE>
 __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u16* slut, u64 p1_in) {
+  constexpr bool kPair = MODE == 2, kBlk = MODE == 1;
   using S = WS<TIn>;
   constexpr int CH = S::CH, TILE = S::TILE, TPL1 = S::TPL1;
   constexpr int WPC = CH * (int)sizeof(TC) / 4;
   constexpr int NTILE_LOG = WS<TC>::LOG;  // next level's tile (its input = codes)
   const int lane = threadIdx.x & 31;
-  const bool scatter = P.out != nullptr;
+  const bool scatter = kPair || P.out != nullptr;
   const u8* in = reinterpret_cast<const u8*>(P.in);
   const u32 l2_chunks = (1u << P.l2_log) / CH;
   uint4 q[S::K];
@@ -363,16 +364,27 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
             const u64 dst = bt ? (u64)__ldg(&ne->one_base) + P1 + r1
                                : (u64)__ldg(&ne->zero_base) + (t0 + e + j - P1 - r1);
             if (dst < P.m_next) {
-              gout[dst] = (TC)v;
-              if ((v >> sh1) & 1u) tf = (u32)(dst >> NTILE_LOG);
+              if (kPair) {  // the last level's bit at its position (region zeroed)
+                if ((v >> sh1) & 1u) {
+                  atomicOr(reinterpret_cast<u32*>(P.next_words) + (dst >> 5), 1u << (dst & 31));
+                  tf = (u32)(dst >> 16);
+                }
+              } else {
+                gout[dst] = (TC)v;
+                if ((v >> sh1) & 1u) tf = (u32)(dst >> (kBlk ? 16 : NTILE_LOG));
+              }
             }
             r1 += bt;
           }
           const u32 key = tf != 0xffffffffu ? tf : 0x80000000u | (u32)lane;  // unique if none
           const unsigned peers = __match_any_sync(FULLM, key);
           if (tf != 0xffffffffu && lane == __ffs(peers) - 1) {
-            atomicAdd(P.next_tile_counts + tf, (u32)__popc(peers));
-            atomicAdd(P.next_l1_counts + (((u64)tf << NTILE_LOG) >> 16), (u32)__popc(peers));
+            if (kPair || kBlk) {  // per L1 block only
+              atomicAdd(P.next_l1_counts + tf, (u32)__popc(peers));
+            } else {
+              atomicAdd(P.next_tile_counts + tf, (u32)__popc(peers));
+              atomicAdd(P.next_l1_counts + (((u64)tf << NTILE_LOG) >> 16), (u32)__popc(peers));
+            }
           }
         }
       }
@@ -581,14 +593,65 @@ __device__ __forceinline__ void wcount_tile(const u8* stage, u32 Z, u32 zoff, u6
     if (cc) {
       const u64 tf = ((one ? odst : zdst) >> tile_log) + seg;
       atomicAdd(tcounts + tf, cc);
-      atomicAdd(l1counts + ((tf << tile_log) >> 16), cc);
+      if (l1counts) atomicAdd(l1counts + ((tf << tile_log) >> 16), cc);
     }
   }
 }
 
-template <typename TIn, typename TC, bool kLut>
+// Pair mode: the staged run of `cnt` codes at stage byte `soff` (soff = dst *
+// sizeof(TC) mod 16) lands at positions [dst, dst + cnt) of the LAST level,
+// whose bits are the codes' bit `sh`.  Every aligned 16-byte chunk of the
+// staging is one aligned 16-bit (u8 codes) / 8-bit (u16) piece of that
+// level's bit-vector: one SWAR gather per chunk, plain stores for the chunks
+// inside the run, atomicOr for its (partial) first / last chunk -- the
+// neighbouring runs own the other bits of those words (region zeroed before
+// the launch).  The run's ones are added to the level's per-L1-block counts
+// (a run of <= 4096 codes crosses at most one block boundary).
+template <typename TC>
+__device__ __forceinline__ void wpair_bits(const u8* stage, u32 cnt, u32 soff, u64 dst, u32 sh,
+                                           u64* nwords, u32* l1counts, int lane) {
+  constexpr u32 SZ = sizeof(TC), EPC = 16 / SZ;
+  const u32 h = (soff & 15u) / SZ;  // chunk 0 elements before the run
+  const u32 nch = (h + cnt + EPC - 1) / EPC;
+  const u64 g0 = dst - h;           // chunk 0's first position (a multiple of EPC)
+  const u8* base = stage + (soff & ~15u);
+  const u64 bnd = ((dst >> 16) + 1) << 16;
+  constexpr u32 FULLC = (1u << EPC) - 1u;
+  u32 clo = 0, chi = 0;
+  for (u32 c = lane; c < nch; c += 32) {
+    const uint4 q = *reinterpret_cast<const uint4*>(base + 16 * c);
+    const u32 cw[4] = {q.x, q.y, q.z, q.w};
+    u32 m = wmask<TC, 4>(cw, sh);
+    const u32 lo = c == 0 ? h : 0u;
+    const u32 hi = min(EPC, h + cnt - c * EPC);
+    const u32 vm = (FULLC >> (EPC - hi)) & ~((1u << lo) - 1u);
+    m &= vm;
+    const u64 g = g0 + (u64)c * EPC;
+    if (vm == FULLC) {
+      if (SZ == 1)
+        reinterpret_cast<u16*>(nwords)[g >> 4] = (u16)m;
+      else
+        reinterpret_cast<u8*>(nwords)[g >> 3] = (u8)m;
+    } else if (m) {
+      atomicOr(reinterpret_cast<u32*>(nwords) + (g >> 5), m << (u32)(g & 31));
+    }
+    if (g >= bnd) chi += __popc(m); else clo += __popc(m);
+  }
+  u32 x = clo | (chi << 16);  // <= 4096 each
+#pragma unroll
+  for (int d = 16; d; d >>= 1) x += __shfl_xor_sync(FULLM, x, d);
+  if (lane == 0 && (x & 0xffffu)) atomicAdd(l1counts + (dst >> 16), x & 0xffffu);
+  if (lane == 1 && (x >> 16)) atomicAdd(l1counts + (bnd >> 16), x >> 16);
+}
+
+// MODE 0: next level counted per tile and per L1 block (tile mode); 1 (kBlk):
+// this and the next level in block mode -- next-level ones counted per run in
+// pass 1 (the staged runs are re-read only for a run crossing an L1 block);
+// 2 (kPair): the next level is the last, its bits written from the staging.
+template <typename TIn, typename TC, bool kLut, int MODE>
 __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 4 KiB tiles: smem allows 4 CTAs
     wlevel_kernel(const __grid_constant__ WLevelParams P) {
+  constexpr bool kPair = MODE == 2, kBlk = MODE == 1;
   using S = WS<TIn>;
   using F = WF<TIn, TC>;
   constexpr int TILE = S::TILE, TPL1 = S::TPL1;
@@ -617,6 +680,18 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
   const u32 ntiles = (u32)((P.m + TILE - 1) / TILE);
   const u32 nfull = (u32)(P.m / TILE);
   const u32 gw = blockIdx.x * W_WARPS + warp, nw = gridDim.x * W_WARPS;
+  // kBlk at a LUT level 0: per-lane SIMD copies of the next bit's thresholds
+  // (a threshold above every symbol value never compares true: enable mask 0)
+  u32 nt[3] = {0, 0, 0}, ne[3] = {0, 0, 0};
+  if (kBlk && kLut) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const u32 tv = P.nthr[i];
+      const bool on = tv <= (sizeof(TIn) == 1 ? 0xffu : 0xffffu);
+      nt[i] = on ? tv * (sizeof(TIn) == 1 ? 0x01010101u : 0x00010001u) : 0u;
+      ne[i] = on ? 0xffffffffu : 0u;
+    }
+  }
   // Block mode (level 0 of a large u8 text, tile_counts == nullptr): a warp
   // takes whole L1 blocks and walks their tiles in order, so P1 is the L1
   // entry plus the warp's own running count -- no per-tile counting pass.
@@ -625,7 +700,7 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
     return blockm ? (gw + (i / TPL1) * nw) * TPL1 + i % TPL1 : gw + i * nw;
   };
   u32 run = 0;  // block mode: ones of the block's tiles before this one
-  const bool scatter = P.out != nullptr;
+  const bool scatter = kPair || P.out != nullptr;
   const u8* in = reinterpret_cast<const u8*>(P.in);
 
   if (lane == 0) {
@@ -646,7 +721,7 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
     const u32 tnext = tile_at(it + W_RING);  // the tile this ring slot streams next
     if (blockm && t % TPL1 == 0) run = 0;
     if (t >= nfull) {  // the partial last tile
-      general_tile<TIn, TC, kLut>(P, t, slut, blockm ? __ldg(P.l1 + t / TPL1) + run : ~0ull);
+      general_tile<TIn, TC, kLut, MODE>(P, t, slut, blockm ? __ldg(P.l1 + t / TPL1) + run : ~0ull);
       if (scatter && lane == 0) w_bulk_commit();  // keep one bulk group per tile
       continue;
     }
@@ -701,7 +776,7 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
       __syncwarp();
       if (lane == 0 && tnext < nfull)
         w_load_tile(ring + slot * TB, in + (u64)tnext * TB, TB, &mbar[slot]);
-      general_tile<TIn, TC, kLut>(P, t, slut, blockm ? l1v + run : ~0ull);
+      general_tile<TIn, TC, kLut, MODE>(P, t, slut, blockm ? l1v + run : ~0ull);
       if (lane == 0) w_bulk_commit();  // keep one bulk group per tile
       continue;
     }
@@ -713,18 +788,32 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
 
     // ---- pass 1: masks and counts per row ------------------------------------
     u32 mrow[ROWS];
+    u32 zc = 0, oc = 0;  // kBlk: next-level ones bound for the zeros / ones run
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
       u32 v[LW];
       wrow_load<LW>(tin + r * RB + lane * LB, v);
+      u32 nm = 0;  // kBlk: the next level's bit of each element
       if (kLut) {
         // level 0 through the LUT: the level bit is the TOP code bit, i.e.
         // `symbol >= thr` (codes are monotone in symbols) -- a SIMD compare
-        // of the raw symbols, no table lookups in this pass
+        // of the raw symbols, no table lookups in this pass; the next bit is
+        // the parity of (symbol >= nthr[i]) over the three thresholds of the
+        // codes' top two bits
         if (sizeof(TIn) == 1) {
           const u32 t4 = P.thr * 0x01010101u;
           const u32 y0 = __vcmpgeu4(v[0], t4) & 0x01010101u, y1 = __vcmpgeu4(v[LW - 1], t4) & 0x01010101u;
           mrow[r] = P.thr > 0xffu ? 0u : ((y1 * 16u + y0) * 0x01020408u) >> 24;
+          if (kBlk) {
+            u32 y[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const u32 x = v[i % LW];
+              y[i] = ((__vcmpgeu4(x, nt[0]) & ne[0]) ^ (__vcmpgeu4(x, nt[1]) & ne[1]) ^
+                      (__vcmpgeu4(x, nt[2]) & ne[2])) & 0x01010101u;
+            }
+            nm = ((y[1] * 16u + y[0]) * 0x01020408u) >> 24;
+          }
         } else {
           const u32 t2 = P.thr * 0x00010001u;
           u32 mm = 0;
@@ -733,6 +822,17 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
             const u32 y0 = __vcmpgeu2(v[i], t2) & 0x00010001u, y1 = __vcmpgeu2(v[i + 1], t2) & 0x00010001u;
             const u32 z = y1 * 4u + y0;  // bits 0, 16, 2, 18 -> elements 0, 1, 2, 3
             mm |= ((z | (z >> 15)) & 0xfu) << (2 * i);
+            if (kBlk) {
+              u32 y[2];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const u32 x = v[i + h];
+                y[h] = ((__vcmpgeu2(x, nt[0]) & ne[0]) ^ (__vcmpgeu2(x, nt[1]) & ne[1]) ^
+                        (__vcmpgeu2(x, nt[2]) & ne[2])) & 0x00010001u;
+              }
+              const u32 zn = y[1] * 4u + y[0];
+              nm |= ((zn | (zn >> 15)) & 0xfu) << (2 * i);
+            }
           }
           mrow[r] = P.thr > 0xffffu ? 0u : mm;
         }
@@ -740,6 +840,11 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
         u32 cw[WR];
         wrow_codes<TIn, TC, kLut>(v, slut, P.lut, cw);
         mrow[r] = wmask<TC, WR>(cw, P.shift_bit);
+        if (kBlk) nm = wmask<TC, WR>(cw, P.shift_bit - 1);
+      }
+      if (kBlk) {
+        zc += __popc(nm & ~mrow[r] & 0xffu);
+        oc += __popc(nm & mrow[r]);
       }
     }
     u32 r1[ROWS], rtot[ROWS];
@@ -960,6 +1065,17 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
       // the input slot is free: the tile three ahead streams into it
       if (lane == 0 && tnext < nfull)
         w_load_tile(ring + slot * TB, in + (u64)tnext * TB, TB, &mbar[slot]);
+      if (kPair) {
+        // the last level's bits straight from the staged runs
+        const u32 sh1 = P.shift_bit - 1;
+        if (zlive) wpair_bits<TC>(stage, zerosA, zoff, zdst, sh1, P.next_words, P.next_l1_counts, lane);
+        if (olive) wpair_bits<TC>(stage, onesA, ooff, odst, sh1, P.next_words, P.next_l1_counts, lane);
+        if (kTwoSeg && split < (u32)TILE) {
+          if (zliveB) wpair_bits<TC>(stage, zerosB, zoffB, zdstB, sh1, P.next_words, P.next_l1_counts, lane);
+          if (oliveB) wpair_bits<TC>(stage, onesB, ooffB, odstB, sh1, P.next_words, P.next_l1_counts, lane);
+        }
+        continue;
+      }
       u8* gout = reinterpret_cast<u8*>(P.out);
 #pragma unroll
       for (int rr = 0; rr < 4; ++rr) {
@@ -982,6 +1098,27 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
         }
         if (lane == 0 && body) w_bulk_s2g(gout + db + head, stage + soff + head, body);
       }
+      if (kBlk) {
+        // next level's ones per L1 block: the pass-1 counts of each run, unless
+        // the run crosses a block boundary (or the tile holds two nodes: its
+        // pass-1 counts are not split by node) -- then the staged runs
+        const bool two = kTwoSeg && split < (u32)TILE;
+        const bool zx = zlive && ((zdst & 0xffffu) + zerosA > 65536u);
+        const bool ox = olive && ((odst & 0xffffu) + onesA > 65536u);
+        if (two || zx || ox) {
+          wcount_tile<TC, false>(stage, zlive ? zerosA : 0u, zoff, zdst, olive ? onesA : 0u, ooff, odst,
+                                 P.shift_bit - 1, 16, P.next_l1_counts, nullptr, lane);
+          if (two)
+            wcount_tile<TC, false>(stage, zliveB ? zerosB : 0u, zoffB, zdstB, oliveB ? onesB : 0u, ooffB,
+                                   odstB, P.shift_bit - 1, 16, P.next_l1_counts, nullptr, lane);
+        } else {
+          u32 x = zc | (oc << 16);  // <= 4096 each
+#pragma unroll
+          for (int d = 16; d; d >>= 1) x += __shfl_xor_sync(FULLM, x, d);
+          if (lane == 0 && zlive && (x & 0xffffu)) atomicAdd(P.next_l1_counts + (zdst >> 16), x & 0xffffu);
+          if (lane == 1 && olive && (x >> 16)) atomicAdd(P.next_l1_counts + (odst >> 16), x >> 16);
+        }
+      } else {
       // next level's ones of both runs per next-level tile (<= 3 per run) and
       // L1 block, in one pass over the staged tile
       wcount_tile<TC, (WS<TIn>::TILE > WS<TC>::TILE)>(stage, zlive ? zerosA : 0u, zoff, zdst, olive ? onesA : 0u, ooff, odst,
@@ -989,6 +1126,7 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
       if (kTwoSeg && split < (u32)TILE)
         wcount_tile<TC, (WS<TIn>::TILE > WS<TC>::TILE)>(stage, zliveB ? zerosB : 0u, zoffB, zdstB, oliveB ? onesB : 0u, ooffB, odstB,
                         P.shift_bit - 1, NTILE_LOG, P.next_tile_counts, P.next_l1_counts, lane);
+      }
       if (lane == 0) w_bulk_commit();  // one bulk group per scattering fast tile
     } else {
       __syncwarp();
@@ -1282,11 +1420,70 @@ __global__ void __launch_bounds__(1024) l1_scan_kernel(const u32* __restrict__ c
   if (tid == 0) *total = carry;
 }
 
+// L2 entries and select samples of a level from its bit-vector and L1
+// directory (rankselect.py:495-532; the level a pair-mode launch wrote): one
+// warp per 65536-bit L1 block, 64 words per step (one 16-byte load per lane),
+// a warp scan of the word-pair popcounts gives every L2 prefix.
+constexpr int D_NT = 256;
+__global__ void __launch_bounds__(D_NT) dir_kernel(const __grid_constant__ DirParams P) {
+  const int lane = threadIdx.x & 31;
+  const u64 nw = (P.m + 63) >> 6;
+  const u64 nblk = (P.m + kL1Bits - 1) / kL1Bits;
+  const u64 l2w = ((1ull << P.l2_log) >> 6) - 1;  // L2 block = l2w + 1 words
+  for (u64 b = (u64)blockIdx.x * (D_NT / 32) + (threadIdx.x >> 5); b < nblk;
+       b += (u64)gridDim.x * (D_NT / 32)) {
+    const u64 l1v = __ldg(P.l1 + b);
+    u32 carry = 0;  // ones of the block before this step
+    for (u64 s = b * (kL1Bits / 64); s < (b + 1) * (kL1Bits / 64) && s < nw; s += 64) {
+      const u64 wi = s + 2 * (u64)lane;
+      ulonglong2 v = make_ulonglong2(0ull, 0ull);
+      if (wi + 1 < nw)
+        v = __ldg(reinterpret_cast<const ulonglong2*>(P.words + wi));
+      else if (wi < nw)
+        v.x = __ldg(P.words + wi);
+      const u32 c0 = __popcll(v.x), c = c0 + __popcll(v.y);
+      u32 inc = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u32 y = __shfl_up_sync(FULLM, inc, d);
+        if (lane >= d) inc += y;
+      }
+      const u32 ex = carry + inc - c;  // ones of the block before word wi
+      carry += __shfl_sync(FULLM, inc, 31);
+      if (wi >= nw) continue;
+      if ((wi & l2w) == 0) P.l2[(wi << 6) >> P.l2_log] = (u16)ex;
+      if (wi + 1 < nw && ((wi + 1) & l2w) == 0) P.l2[((wi + 1) << 6) >> P.l2_log] = (u16)(ex + c0);
+      // select samples: every rate-th one / zero (1-based ordinals)
+      const u64 ob = l1v + ex;
+      for (u64 qo = wnext_multiple(ob, P.rate, P.rate_log); qo <= ob + c; qo += P.rate) {
+        const u32 k = (u32)(qo - ob);
+        const u64 pos = k <= c0 ? (wi << 6) + select_in_word64(v.x, k)
+                                : ((wi + 1) << 6) + select_in_word64(v.y, k - c0);
+        const u64 si = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
+        if (si < P.ones_cap) P.ones[si] = pos;
+      }
+      const u64 valid = min((u64)128, P.m - (wi << 6));
+      const u64 zb = (wi << 6) - ob;
+      const u64 zm0 = ~v.x & (valid >= 64 ? ~0ull : (1ull << valid) - 1);
+      const u64 zm1 = valid <= 64 ? 0ull : ~v.y & (valid >= 128 ? ~0ull : (1ull << (valid - 64)) - 1);
+      const u32 z0 = __popcll(zm0), zc = z0 + __popcll(zm1);
+      for (u64 qo = wnext_multiple(zb, P.rate, P.rate_log); qo <= zb + zc; qo += P.rate) {
+        const u32 k = (u32)(qo - zb);
+        const u64 pos = k <= z0 ? (wi << 6) + select_in_word64(zm0, k)
+                                : ((wi + 1) << 6) + select_in_word64(zm1, k - z0);
+        const u64 si = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
+        if (si < P.zeros_cap) P.zeros[si] = pos;
+      }
+    }
+  }
+}
+
 namespace {
-template <typename TIn, typename TC, bool kLut>
+template <typename TIn, typename TC, bool kLut, int MODE>
 cudaError_t launch_w(const WLevelParams& p, int sms, cudaStream_t st) {
+  constexpr bool kPair = MODE == 2;
   const size_t smem = 512 + (size_t)W_WARPS * WF<TIn, TC>::WARP_SMEM;
-  auto kern = wlevel_kernel<TIn, TC, kLut>;
+  auto kern = wlevel_kernel<TIn, TC, kLut, MODE>;
   // attribute + occupancy once per device (host cost off the per-level path)
   // (per device: attributes and occupancy belong to a device context;
   // racing first calls only repeat idempotent work)
@@ -1305,7 +1502,7 @@ cudaError_t launch_w(const WLevelParams& p, int sms, cudaStream_t st) {
     if (dev_ok) cached[dev].store(per_sm, std::memory_order_release);
   }
   const u64 tiles = (p.m + WS<TIn>::TILE - 1) / WS<TIn>::TILE;
-  if (!p.out) {  // the last level: no partition
+  if (!p.out && !kPair) {  // the last level: no partition
     u64 blocks = (tiles + 7) / 8;
     if (blocks > (u64)sms * 8) blocks = (u64)sms * 8;
     const int lsmem = 8 * (2 * WS<TIn>::BYTES + 16);
@@ -1327,16 +1524,26 @@ cudaError_t launch_w(const WLevelParams& p, int sms, cudaStream_t st) {
 }
 }  // namespace
 
+namespace {
+template <int MODE>
+cudaError_t launch_wlevel_t(const WLevelParams& p, int in_bytes, int code_bytes, bool lut, int sms,
+                            cudaStream_t st) {
+  if (in_bytes == 1 && code_bytes == 1)
+    return lut ? launch_w<u8, u8, true, MODE>(p, sms, st) : launch_w<u8, u8, false, MODE>(p, sms, st);
+  if (in_bytes == 1 && code_bytes == 2) return launch_w<u8, u16, true, MODE>(p, sms, st);
+  if (in_bytes == 2 && code_bytes == 1) return launch_w<u16, u8, true, MODE>(p, sms, st);
+  if (in_bytes == 2 && code_bytes == 2)
+    return lut ? launch_w<u16, u16, true, MODE>(p, sms, st) : launch_w<u16, u16, false, MODE>(p, sms, st);
+  return cudaErrorInvalidValue;
+}
+}  // namespace
+
 cudaError_t launch_wlevel(const WLevelParams& p, int in_bytes, int code_bytes, bool lut, int sms,
                           cudaStream_t st) {
   if (p.m == 0) return cudaSuccess;
-  if (in_bytes == 1 && code_bytes == 1)
-    return lut ? launch_w<u8, u8, true>(p, sms, st) : launch_w<u8, u8, false>(p, sms, st);
-  if (in_bytes == 1 && code_bytes == 2) return launch_w<u8, u16, true>(p, sms, st);
-  if (in_bytes == 2 && code_bytes == 1) return launch_w<u16, u8, true>(p, sms, st);
-  if (in_bytes == 2 && code_bytes == 2)
-    return lut ? launch_w<u16, u16, true>(p, sms, st) : launch_w<u16, u16, false>(p, sms, st);
-  return cudaErrorInvalidValue;
+  if (p.next_words) return launch_wlevel_t<2>(p, in_bytes, code_bytes, lut, sms, st);
+  if (p.next_block) return launch_wlevel_t<1>(p, in_bytes, code_bytes, lut, sms, st);
+  return launch_wlevel_t<0>(p, in_bytes, code_bytes, lut, sms, st);
 }
 
 cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, u32 thr, u32* tile_counts,
@@ -1352,6 +1559,15 @@ cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, u32 thr, u32* 
   return cudaGetLastError();
 }
 
+cudaError_t launch_dir(const DirParams& p, int sms, cudaStream_t st) {
+  if (p.m == 0) return cudaSuccess;
+  const u64 nblk = (p.m + kL1Bits - 1) / kL1Bits;
+  u64 blocks = (nblk + (D_NT / 32) - 1) / (D_NT / 32);
+  if (blocks > (u64)sms * 8) blocks = (u64)sms * 8;
+  dir_kernel<<<(unsigned)blocks, D_NT, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_l1_scan(const u32* counts, u64 n_l1, u64* l1, u64* total, cudaStream_t st) {
   l1_scan_kernel<<<1, 1024, 0, st>>>(counts, n_l1, l1, total);
   return cudaGetLastError();
@@ -1360,7 +1576,7 @@ cudaError_t launch_l1_scan(const u32* counts, u64 n_l1, u64* l1, u64* total, cud
 u64 wlevel_warp_slots(int sms) {
   int per_sm = 1;
   const size_t smem = 512 + (size_t)W_WARPS * WF<u8, u8>::WARP_SMEM;
-  auto kern = wlevel_kernel<u8, u8, false>;
+  auto kern = wlevel_kernel<u8, u8, false, 0>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W_NT, smem) != cudaSuccess) {
     cudaGetLastError();

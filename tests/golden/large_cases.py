@@ -108,7 +108,9 @@ def zipf_torch(seed: int, sigma: int, n: int, device, chunk: int = 1 << 26):
         z = splitmix_torch(seed, lo, hi, device)
         u = ((z >> 11) & ((1 << 53) - 1)).to(torch.float64) * 2.0 ** -53
         s = torch.searchsorted(cdf, u, right=True)
-        out[lo:hi] = s.to(torch.int32).to(torch.int16)  # values < 2^16: bit pattern of u16
+        # values < 2^16 as the int16 holding the same u16 bit pattern: shift
+        # into int16's range first (a CUDA int32 -> int16 cast saturates)
+        out[lo:hi] = torch.where(s >= 32768, s - 65536, s).to(torch.int16)
     return out
 
 

@@ -4,6 +4,8 @@ the symbol -> code map), u8 / u16 codes.  Every array of the device tree is
 compared with the oracle (the numpy restatement pinned to the reference's
 golden vectors), then batched queries are checked against the text."""
 
+import io
+
 import numpy as np
 import pytest
 
@@ -337,3 +339,38 @@ def test_single_level_trees(W, dt, syms):
     assert t.num_levels == 1
     assert_same_structure(t, O.build(text))
     _check_queries(W, t, text, t.alphabet.sorted_symbols, m=3000)
+
+
+PAIR_CASES = {
+    "u8_s256": lambda: np.random.default_rng(31).integers(0, 256, (1 << 22) + 4097, dtype=np.uint8),
+    "u8_s4_small": lambda: np.random.default_rng(32).integers(0, 4, 70_001, dtype=np.uint8),
+    "dna": lambda: np.frombuffer(b"ACGT", np.uint8)[
+        np.random.default_rng(33).integers(0, 4, (1 << 22) + 13)],
+    "u8_s16_skewed": lambda: np.minimum(np.random.default_rng(34).geometric(0.3, 1 << 21), 16)
+                                .astype(np.uint8) - 1,
+    "u16_s65536": lambda: np.random.default_rng(35).integers(0, 65536, (1 << 21) + 9)
+                             .astype(np.uint16),
+    "u16_s1024_lut": lambda: (np.random.default_rng(36).integers(0, 1024, (1 << 20) + 1)
+                              * 37).astype(np.uint16),
+    "u16_zipf": lambda: _zipf((1 << 21) + 5, 65536, seed=37),
+}
+
+
+@pytest.mark.parametrize("block", ["0", "1"])
+@pytest.mark.parametrize("name", sorted(PAIR_CASES))
+def test_pair_mode_matches_level_by_level(W, name, block, monkeypatch):
+    """Pair mode (the last two levels in one pass: the last level's bits from
+    the staged runs, its L2 / samples from dir_kernel) builds the same index
+    as the level-by-level path (WT_PAIR=0), and the oracle's."""
+    text = PAIR_CASES[name]()
+    monkeypatch.setenv("WT_BLOCK_MODE", block)
+    monkeypatch.setenv("WT_PAIR", "1")
+    t1 = W.construct(text)
+    monkeypatch.setenv("WT_PAIR", "0")
+    t0 = W.construct(text)
+    b1, b0 = io.BytesIO(), io.BytesIO()
+    t1.save(b1)
+    t0.save(b0)
+    assert b1.getvalue() == b0.getvalue()
+    assert_same_structure(t1, O.build(text))
+    _check_queries(W, t1, text, t1.alphabet.sorted_symbols, m=5000)

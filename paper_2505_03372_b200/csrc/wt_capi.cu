@@ -676,8 +676,9 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       std::vector<char> blk(P.L, 0);
       {
         const uint64_t slots2 = 2 * wlevel_warp_slots(sm_count(device));
+        const char* bl = getenv("WT_BLK_LEVELS");  // "0": levels >= 1 in tile mode (A/B)
         for (uint32_t l = 0; l < P.L; ++l) {
-          const bool big = bm ? bm[0] == '1' : t->lv[l].meta.n_l1 >= slots2;
+          const bool big = (bm ? bm[0] == '1' : t->lv[l].meta.n_l1 >= slots2) && !(bl && bl[0] == '0');
           blk[l] = l == 0 ? block_mode : (blk[l - 1] && big && l + 1 < P.L);
         }
       }

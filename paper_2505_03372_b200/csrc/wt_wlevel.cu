@@ -205,8 +205,9 @@ __device__ __forceinline__ u64 wnext_multiple(u64 o, u64 rate, int rate_log) {
 // Any tile the fast path does not take (the level's partial last tile, tiles
 // spanning several nodes): loads from global memory, element-by-element
 // destination stores, per-element next-level counts.
+// returns the tile's ones (block mode: the caller's running count)
 template <typename TIn, typename TC, bool kLut, int MODE>
-__device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u16* slut, u64 p1_in) {
+__device__ __noinline__ u32 general_tile(const WLevelParams& P, u32 t, const u16* slut, u64 p1_in) {
   constexpr bool kPair = MODE == 2, kBlk = MODE == 1;
   using S = WS<TIn>;
   constexpr int CH = S::CH, TILE = S::TILE, TPL1 = S::TPL1;
@@ -343,7 +344,7 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
       }
     }
 
-    if (!scatter) return;
+    if (!scatter) return tile_ones;
 
     {
       TC* gout = reinterpret_cast<TC*>(P.out);
@@ -389,6 +390,7 @@ __device__ __noinline__ void general_tile(const WLevelParams& P, u32 t, const u1
         }
       }
     }
+    return tile_ones;
 }
 
 // ---------------------------------------------------------------------------
@@ -776,7 +778,7 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
       __syncwarp();
       if (lane == 0 && tnext < nfull)
         w_load_tile(ring + slot * TB, in + (u64)tnext * TB, TB, &mbar[slot]);
-      general_tile<TIn, TC, kLut, MODE>(P, t, slut, blockm ? l1v + run : ~0ull);
+      run += general_tile<TIn, TC, kLut, MODE>(P, t, slut, blockm ? l1v + run : ~0ull);
       if (lane == 0) w_bulk_commit();  // keep one bulk group per tile
       continue;
     }

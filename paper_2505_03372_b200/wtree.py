@@ -78,6 +78,9 @@ def _device_text(text):
         raise BuildError(f"unsupported device text dtype {text.dtype}")
     if not text.is_contiguous():
         raise BuildError("device text must be contiguous")
+    # the build runs on its own (non-blocking) stream: kernels still producing
+    # the text on the caller's stream must finish first
+    torch.cuda.current_stream(text.device).synchronize()
     return text.data_ptr(), int(text.numel()), sb
 
 

@@ -705,6 +705,8 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       // (WT_PAIR=0 turns it off: the parity tests run both.)
       const char* pe = getenv("WT_PAIR");
       const bool pair_ok = !(pe && pe[0] == '0');
+      const char* de = getenv("WT_DIR");
+      const bool dir_after = !(de && de[0] == '0');
       int ci = 0;
       for (uint32_t l = 0; l < P.L; ++l) {
         const uint64_t m = (uint64_t)P.sizes[l];
@@ -753,7 +755,26 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
         wp.l2_log = l2_log;
         wp.rate_log = rate_log_of(sample_rate);
         wp.rate = sample_rate;
+        // L2 entries / samples of a partitioning level by dir_kernel after the
+        // launch (a streaming pass over its bits) instead of inside the level
+        // kernel (WT_DIR=0: inside)
+        wp.skip_dir = dir_after && wp.out ? 1 : 0;
         CU(launch_wlevel(wp, in_bytes, P.code_bytes, l == 0 && dlut != nullptr, sm_count(device), st));
+        if (wp.skip_dir) {
+          DirParams dp{};
+          dp.words = wp.words;
+          dp.m = m;
+          dp.l1 = h.l1;
+          dp.l2 = h.l2;
+          dp.ones = h.ones;
+          dp.zeros = h.zeros;
+          dp.ones_cap = m / sample_rate;
+          dp.zeros_cap = m / sample_rate;
+          dp.l2_log = l2_log;
+          dp.rate_log = rate_log_of(sample_rate);
+          dp.rate = sample_rate;
+          CU(launch_dir(dp, sm_count(device), st));
+        }
         ci ^= 1;
         if (pair) {  // the last level: L1 from the pair pass's counts, then L2 + samples
           LevelHost& hn = t->lv[l + 1];
@@ -1264,6 +1285,7 @@ typedef int (*nccl_bcast_t)(const void*, void*, size_t, int, int, ncclComm_t, cu
 typedef int (*nccl_destroy_t)(ncclComm_t);
 typedef const char* (*nccl_errstr_t)(int);
 typedef int (*nccl_group_t)(void);
+typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
 
 struct NcclApi {
   bool ok = false;
@@ -1273,6 +1295,7 @@ struct NcclApi {
   nccl_destroy_t destroy;
   nccl_errstr_t errstr;
   nccl_group_t group_start, group_end;
+  nccl_allreduce_t allreduce;
 };
 static NcclApi g_nccl;
 static std::once_flag g_nccl_once;
@@ -1288,8 +1311,9 @@ static int nccl_load() {
     g_nccl.errstr = (nccl_errstr_t)dlsym(h, "ncclGetErrorString");
     g_nccl.group_start = (nccl_group_t)dlsym(h, "ncclGroupStart");
     g_nccl.group_end = (nccl_group_t)dlsym(h, "ncclGroupEnd");
+    g_nccl.allreduce = (nccl_allreduce_t)dlsym(h, "ncclAllReduce");
     g_nccl.ok = g_nccl.get_uid && g_nccl.init_rank && g_nccl.bcast && g_nccl.destroy &&
-                g_nccl.group_start && g_nccl.group_end;
+                g_nccl.group_start && g_nccl.group_end && g_nccl.allreduce;
   });
   if (!g_nccl.ok) return fail(WT_ERR_NCCL, "libnccl.so.2 not loadable");
   return WT_OK;
@@ -1360,15 +1384,16 @@ extern "C" int wt_tree_replicate(wt_tree* root_tree, const uint8_t id[128], int 
   cudaFree(dh);
   // 2. receivers allocate an identically shaped tree
   wt_tree* t = nullptr;
+  int alloc_rc = WT_OK;
   if (rank == 0) {
     t = root_tree;
+  } else if (!(t = new wt_tree()) ||
+             cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete t;
+    t = nullptr;
+    alloc_rc = fail(WT_ERR_CUDA, "stream create failed");  // reported after the status reduce
   } else {
-    t = new wt_tree();
     t->device = device;
-    if (cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking) != cudaSuccess) {
-      delete t;
-      return fail(WT_ERR_CUDA, "stream create failed");
-    }
     memcpy(&t->meta, hdr.data(), sizeof(wt_meta));
     t->meta.device = (uint32_t)device;
     Plan& P = t->plan;
@@ -1382,39 +1407,75 @@ extern "C" int wt_tree_replicate(wt_tree* root_tree, const uint8_t id[128], int 
     for (uint32_t i = 0; i < P.sigma; ++i) P.hist[i] = cum[i + 1] - cum[i];
     plan_codes(P);
     plan_shape(P, t->meta.l2_bits);
-    int rc = alloc_tree(t, st);
-    if (rc != WT_OK) {
+    alloc_rc = alloc_tree(t, st);
+    if (alloc_rc == WT_OK)
+      for (uint32_t l = 0; l < P.L; ++l)
+        memcpy(&t->lv[l].meta, hdr.data() + sizeof(wt_meta) + l * sizeof(wt_level_meta),
+               sizeof(wt_level_meta));
+  }
+  // every rank learns whether every receiver has its tree before any rank
+  // enters the grouped broadcast (a rank that returned early would leave the
+  // others blocked in the collective): max-reduce of the allocation status
+  auto drop = [&]() {
+    if (rank != 0 && t) {
       free_tree_arrays(t);
       delete t;
-      return rc;
+      t = nullptr;
     }
-    for (uint32_t l = 0; l < P.L; ++l)
-      memcpy(&t->lv[l].meta, hdr.data() + sizeof(wt_meta) + l * sizeof(wt_level_meta),
-             sizeof(wt_level_meta));
+  };
+  {
+    int* dst_flag = nullptr;
+    int any = alloc_rc != WT_OK ? 1 : 0;
+    cudaError_t ce = cudaMalloc(&dst_flag, 4);
+    if (ce == cudaSuccess) ce = cudaMemcpy(dst_flag, &any, 4, cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) {  // still take part: the others are waiting on this rank
+      any = 1;
+      if (!dst_flag) cudaMalloc(&dst_flag, 4);
+    }
+    const int nr = dst_flag ? g_nccl.allreduce(dst_flag, dst_flag, 1, /*ncclInt32*/ 2, /*ncclMax*/ 2, comm, st) : 1;
+    int all = 1;
+    if (nr == 0 && cudaMemcpyAsync(&all, dst_flag, 4, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+        cudaStreamSynchronize(st) == cudaSuccess) {
+      all = any ? 1 : all;
+    } else {
+      all = 1;
+    }
+    if (dst_flag) cudaFree(dst_flag);
+    if (all) {
+      drop();
+      return alloc_rc != WT_OK ? alloc_rc : fail(WT_ERR_CUDA, "replicate: a receiver could not allocate its tree");
+    }
   }
-  // 3. bulk arrays, one grouped broadcast
-  cudaEvent_t e0, e1;
-  CU(cudaEventCreate(&e0));
-  CU(cudaEventCreate(&e1));
-  CU(cudaEventRecord(e0, st));
-  NC(g_nccl.group_start());
-  NC(g_nccl.bcast(t->words, t->words, t->plan.n_words * 8, 1, 0, comm, st));
-  for (uint32_t l = 0; l < t->plan.L; ++l) {
-    LevelHost& h = t->lv[l];
-    if (h.meta.n_l1) NC(g_nccl.bcast(h.l1, h.l1, h.meta.n_l1 * 8, 1, 0, comm, st));
-    if (h.meta.n_l2) NC(g_nccl.bcast(h.l2, h.l2, h.meta.n_l2 * 2, 1, 0, comm, st));
-    if (h.meta.n_ones) NC(g_nccl.bcast(h.ones, h.ones, h.meta.n_ones * 8, 1, 0, comm, st));
-    if (h.meta.n_zeros) NC(g_nccl.bcast(h.zeros, h.zeros, h.meta.n_zeros * 8, 1, 0, comm, st));
-  }
-  NC(g_nccl.group_end());
-  CU(cudaEventRecord(e1, st));
-  CU(cudaStreamSynchronize(st));
-  if (ms_out) cudaEventElapsedTime(ms_out, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  if (rank != 0) {
-    TRY(qlayouts_from_host_totals(t, st));
-    fill_treedev(t);
+  // 3. bulk arrays, one grouped broadcast (a receiver's tree is freed on
+  // any failure from here on)
+  const int rc3 = [&]() -> int {
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    struct EvG { cudaEvent_t a, b; ~EvG() { cudaEventDestroy(a); cudaEventDestroy(b); } } eg{e0, e1};
+    CU(cudaEventRecord(e0, st));
+    NC(g_nccl.group_start());
+    NC(g_nccl.bcast(t->words, t->words, t->plan.n_words * 8, 1, 0, comm, st));
+    for (uint32_t l = 0; l < t->plan.L; ++l) {
+      LevelHost& h = t->lv[l];
+      if (h.meta.n_l1) NC(g_nccl.bcast(h.l1, h.l1, h.meta.n_l1 * 8, 1, 0, comm, st));
+      if (h.meta.n_l2) NC(g_nccl.bcast(h.l2, h.l2, h.meta.n_l2 * 2, 1, 0, comm, st));
+      if (h.meta.n_ones) NC(g_nccl.bcast(h.ones, h.ones, h.meta.n_ones * 8, 1, 0, comm, st));
+      if (h.meta.n_zeros) NC(g_nccl.bcast(h.zeros, h.zeros, h.meta.n_zeros * 8, 1, 0, comm, st));
+    }
+    NC(g_nccl.group_end());
+    CU(cudaEventRecord(e1, st));
+    CU(cudaStreamSynchronize(st));
+    if (ms_out) cudaEventElapsedTime(ms_out, e0, e1);
+    if (rank != 0) {
+      TRY(qlayouts_from_host_totals(t, st));
+      fill_treedev(t);
+    }
+    return WT_OK;
+  }();
+  if (rc3 != WT_OK) {
+    drop();
+    return rc3;
   }
   *out = rank == 0 ? nullptr : t;
   return WT_OK;

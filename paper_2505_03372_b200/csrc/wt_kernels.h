@@ -29,6 +29,7 @@ struct WLevelParams {
   // the first pass; nthr = the three raw-symbol thresholds of the code's top
   // two bits at a LUT level 0 (bit l+1 = parity of symbol >= nthr[i])
   int next_block;
+  int skip_dir;            // L2 entries / samples left to dir_kernel (fast tiles)
   u32 nthr[3];
   u32 thr;                 // level 0 with a LUT: smallest symbol whose code has the top bit
   u32 shift_bit;           // L-1-l

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__
                                                          const i64* __restrict__ ids,
                                                          const i64* __restrict__ args, u64 m,
                                                          bool validate, u32 sym_bits,
-                                                         u32 arg_shift, u32* __restrict__ bucket_of,
+                                                         u32 arg_shift, u32 nb, u32* __restrict__ bucket_of,
                                                          u32* __restrict__ hist, u64 base,
                                                          u64* __restrict__ bad) {
   const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
@@ -250,7 +250,8 @@ __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__
       ok = id >= 0;
       c = ok ? (u32)id : 0u;
     } else {
-      c = (u32)ids[i];
+      const i64 raw = ids[i];
+      c = raw < 0 ? 0u : (u32)min(raw, (i64)T.sigma - 1);  // memory safety only
     }
     if (ok && validate) {
       if (kind == 1) ok = a <= T.n;
@@ -273,6 +274,9 @@ __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__
     }
   }
   if (!ok) atomicMin(bad, base + i);
+  // unvalidated callers promise ids < sigma and in-range arguments; clamp
+  // anyway so a broken promise cannot index past the bucket table
+  bucket = min(bucket, nb - 1u);
   bucket_of[i] = bucket;
   atomicAdd(hist + bucket, 1u);
 }
@@ -454,7 +458,7 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   cudaError_t e = cudaMemsetAsync(S.hist, 0, nb * 4, st);
   if (e != cudaSuccess) return e;
   qsort_key_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(T, kind, ids, args, m, validate, sym_bits,
-                                                      arg_shift, S.bucket_of, S.hist,
+                                                      arg_shift, nb, S.bucket_of, S.hist,
                                                       base, bad);
   const unsigned sb = (nb + QS_PER_CTA - 1) / QS_PER_CTA;
   u32* partial = S.hist + (1u << kQSortMaxBits);

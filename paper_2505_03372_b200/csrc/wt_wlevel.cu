@@ -32,6 +32,7 @@
 // Destination of element j with bit b in node `key`:
 //   b=1: one_base[key] + R1(j)        b=0: zero_base[key] + R0(j)
 #include <atomic>
+#include <cstdlib>
 #include "wt_common.cuh"
 #include "wt_kernels.h"
 
@@ -52,6 +53,10 @@ constexpr int W_NSTAGE = WT_W_NSTAGE;  // staging buffers per warp (1 | 2)
 #define WT_W_MINB 6
 #endif
 constexpr int W_MINB = WT_W_MINB;  // __launch_bounds__ min CTAs per SM
+#ifndef WT_W_MINB4
+#define WT_W_MINB4 4
+#endif
+constexpr int W_MINB4 = WT_W_MINB4;  // the same for 4 KiB tiles (u8 input)
 constexpr unsigned FULLM = 0xffffffffu;
 
 // a warp tile is 2048 elements for both input widths (2 KiB of u8 / 4 KiB
@@ -651,7 +656,7 @@ __device__ __forceinline__ void wpair_bits(const u8* stage, u32 cnt, u32 soff, u
 // pass 1 (the staged runs are re-read only for a run crossing an L1 block);
 // 2 (kPair): the next level is the last, its bits written from the staging.
 template <typename TIn, typename TC, bool kLut, int MODE>
-__global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 4 KiB tiles: smem allows 4 CTAs
+__global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? W_MINB4 : W_MINB)  // 4 KiB tiles: smem allows 4 CTAs
     wlevel_kernel(const __grid_constant__ WLevelParams P) {
   constexpr bool kPair = MODE == 2, kBlk = MODE == 1;
   using S = WS<TIn>;
@@ -791,6 +796,7 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
     // ---- pass 1: masks and counts per row ------------------------------------
     u32 mrow[ROWS];
     u32 zc = 0, oc = 0;  // kBlk: next-level ones bound for the zeros / ones run
+    u32 accT = 0, accO = 0;  // kBlk, codes: per-byte (halfword) next-level ones, of them in the ones run
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
       u32 v[LW];
@@ -842,12 +848,25 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
         u32 cw[WR];
         wrow_codes<TIn, TC, kLut>(v, slut, P.lut, cw);
         mrow[r] = wmask<TC, WR>(cw, P.shift_bit);
-        if (kBlk) nm = wmask<TC, WR>(cw, P.shift_bit - 1);
+        if (kBlk) {  // SIMD byte / halfword counters (<= 32 per field over the tile)
+          const u32 lm = sizeof(TC) == 1 ? 0x01010101u : 0x00010001u;
+#pragma unroll
+          for (int i = 0; i < WR; ++i) {
+            const u32 y = (cw[i] >> P.shift_bit) & lm, nb = (cw[i] >> (P.shift_bit - 1)) & lm;
+            accT += nb;
+            accO += nb & y;
+          }
+        }
       }
-      if (kBlk) {
+      if (kBlk && kLut) {
         zc += __popc(nm & ~mrow[r] & 0xffu);
         oc += __popc(nm & mrow[r]);
       }
+    }
+    if (kBlk && !kLut) {  // fold the SIMD counters
+      const u32 t = sizeof(TC) == 1 ? (accT * 0x01010101u) >> 24 : (accT & 0xffffu) + (accT >> 16);
+      oc = sizeof(TC) == 1 ? (accO * 0x01010101u) >> 24 : (accO & 0xffffu) + (accO >> 16);
+      zc = t - oc;
     }
     u32 r1[ROWS], rtot[ROWS];
 #pragma unroll
@@ -881,6 +900,8 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
     for (int r = 0; r < ROWS; ++r)
       reinterpret_cast<u8*>(P.words)[(t0 >> 3) + r * (RE / 8) + lane] = (u8)mrow[r];
 
+    // L2 entries and samples here, or by dir_kernel after the launch (skip_dir)
+    if (!P.skip_dir) {
     // ---- L2 entries: blocks start at lane-row boundaries (l2_bits >= 64) ------
     if ((1u << P.l2_log) >= (u32)RE) {  // at most one per row: lane r handles row r
       u32 rs = 0;  // ones before row `lane`
@@ -929,6 +950,8 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? 4 : W_MINB)  // 
         }
       }
     }
+
+    }  // !skip_dir
 
     if (scatter) {
       // ---- pass 2: stable partition into the staged zeros / ones runs ----------
@@ -1304,6 +1327,326 @@ __global__ void __launch_bounds__(256) wlast_kernel(const __grid_constant__ WLev
 }
 
 // ---------------------------------------------------------------------------
+// Pair kernel: the last two levels in one pass (every code reaches the last
+// level; WLevelParams::next_words).  Lane i owns the contiguous slice
+// [E i, E i + E) of a warp tile (E = 128 u8 / 64 u16 elements), so its
+// level-l mask is whole u64 words of that level's bit-vector (as in
+// wlast_kernel), and its L2 entries / samples follow from one warp scan.
+// The last level's bits are the next code bit of the tile's zeros-group and
+// ones-group elements, each group in text order (S_{l+1} is the stable
+// partition of S_l): every lane compacts its chunks' next-bit flags with
+// PRMT selectors looked up by the 8-element mask (no byte scatter through
+// shared memory), ORs each chunk's piece into the two group bit-strings in
+// shared memory (its place = the lane's group prefix from the scan + the
+// chunk's prefix inside the slice), and the warp writes the strings to the
+// last level at the groups' destinations (words inside a run stored, the
+// run's first / last word OR-ed: neighbouring runs share them).
+// Chunk k of a lane is read from slice chunk k ^ (lane & 7): the 16-byte
+// reads of a warp spread over all banks.
+// ---------------------------------------------------------------------------
+template <typename TIn, typename TC>
+__device__ __forceinline__ void wp_codes(uint4& q, const u16* slut, const u16* glut, bool lut) {
+  // 16 input bytes -> 16 code bytes (u8 codes) or 8 code halfwords (u16)
+  if (!lut) return;
+  const u32 w[4] = {q.x, q.y, q.z, q.w};
+  u32 o[4] = {0, 0, 0, 0};
+  if (sizeof(TIn) == 1) {  // u8 text, u8 codes (L = 2 here)
+#pragma unroll
+    for (int j = 0; j < 16; ++j) o[j >> 2] |= (u32)slut[(w[j >> 2] >> ((j & 3) * 8)) & 0xffu] << ((j & 3) * 8);
+    q = make_uint4(o[0], o[1], o[2], o[3]);
+  } else if (sizeof(TC) == 1) {  // u16 text, u8 codes: 8 codes in the low 8 bytes
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j >> 2] |= (u32)__ldg(glut + ((w[j >> 1] >> ((j & 1) * 16)) & 0xffffu)) << ((j & 3) * 8);
+    q = make_uint4(o[0], o[1], 0u, 0u);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j >> 1] |= (u32)__ldg(glut + ((w[j >> 1] >> ((j & 1) * 16)) & 0xffffu)) << ((j & 1) * 16);
+    q = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// 8-element flag bytes (bit 0 of each byte = bit `sh` of the element's code)
+// of step s of a code chunk: u8 codes 16 per chunk, u16 codes 8 per chunk
+template <typename TC>
+__device__ __forceinline__ void wp_flags(const uint4& q, int s, u32 sh, u32& f0, u32& f1) {
+  if (sizeof(TC) == 1) {
+    const u32 a = s ? q.z : q.x, b = s ? q.w : q.y;
+    f0 = (a >> sh) & 0x01010101u;
+    f1 = (b >> sh) & 0x01010101u;
+  } else {
+    const u32 a = (q.x >> sh) & 0x00010001u, b = (q.y >> sh) & 0x00010001u;
+    const u32 c = (q.z >> sh) & 0x00010001u, d = (q.w >> sh) & 0x00010001u;
+    f0 = __byte_perm(a, b, 0x6420);
+    f1 = __byte_perm(c, d, 0x6420);
+  }
+}
+
+// bit 0 of 8 flag bytes (elements 0..3 in f0, 4..7 in f1) -> 8-bit mask
+__device__ __forceinline__ u32 wp_gather(u32 f0, u32 f1) {
+  return (((f1 * 16u + f0) * 0x01020408u) >> 24) & 0xffu;
+}
+
+template <typename TIn, typename TC, bool kLut>
+__global__ void __launch_bounds__(256, 2) wpair_kernel(const __grid_constant__ WLevelParams P) {
+  using S = WS<TIn>;
+  constexpr int TILE = S::TILE, TPL1 = S::TPL1, TB = S::BYTES;
+  constexpr int K = S::K;                    // 16-byte chunks per lane (8)
+  constexpr int CE = TILE / 32 / K;          // elements per chunk (16 | 8)
+  constexpr int E = K * CE;                  // elements per lane (128 | 64)
+  constexpr int NW = E / 64;                 // level-l words per lane (2 | 1)
+  constexpr int NS = CE / 8;                 // 8-element steps per chunk (2 | 1)
+  constexpr int GW = TILE / 32 + 2;          // words of one group string (+ alignment)
+  static_assert(K == 8, "chunk rotation assumes 8 chunks per lane");
+  // PRMT selectors compacting the bytes of an 8-element step whose mask bit
+  // is set: selector nibble i = source byte of output byte i
+  __shared__ uint2 csel[256];
+  __shared__ u16 slut[kLut && sizeof(TIn) == 1 ? 256 : 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {
+    u32 lo = 0, hi = 0, n = 0;
+    for (u32 j = 0; j < 8; ++j)
+      if ((tid >> j) & 1) {
+        if (n < 4) lo |= j << (4 * n); else hi |= j << (4 * (n - 4));
+        ++n;
+      }
+    csel[tid] = make_uint2(lo, hi);
+    if (kLut && sizeof(TIn) == 1) slut[tid] = P.lut[tid];
+    __syncthreads();
+  }
+  const u32 ntiles = (u32)((P.m + TILE - 1) / TILE);
+  const u32 nfull = (u32)(P.m / TILE);
+  const u32 gw = blockIdx.x * 8 + warp, nw = gridDim.x * 8;
+  const bool blockm = P.tile_counts == nullptr;
+  auto tile_at = [&](u32 i) -> u32 {
+    return blockm ? (gw + (i / TPL1) * nw) * TPL1 + i % TPL1 : gw + i * nw;
+  };
+  const u8* in = reinterpret_cast<const u8*>(P.in);
+  const u64 l2m = (1ull << P.l2_log) - 1;
+  const u32 sh = P.shift_bit, sh1 = P.shift_bit - 1;
+  extern __shared__ __align__(128) u8 wp_smem[];
+  u8* ring = wp_smem + warp * (2 * TB + 16 + 2 * GW * 4);
+  u64* mbar = reinterpret_cast<u64*>(ring + 2 * TB);
+  u32* gbuf = reinterpret_cast<u32*>(ring + 2 * TB + 16);  // [2][GW]
+  if (lane == 0) {
+    w_mbar_init(&mbar[0]);
+    w_mbar_init(&mbar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (u32 i = 0; i < 2; ++i) {
+      const u32 t = tile_at(i);
+      if (t < nfull) w_load_tile(ring + i * TB, in + (u64)t * TB, TB, &mbar[i]);
+    }
+  }
+  __syncwarp();
+  u32 run = 0, it = 0;
+  for (u32 t = tile_at(0); t < ntiles; t = tile_at(++it)) {
+    const u32 slot = it & 1u;
+    const u32 tnext = tile_at(it + 2);
+    if (blockm && t % TPL1 == 0) run = 0;
+    const u32 b = t / TPL1, tb = t - b * TPL1;
+    const u64 l1v = __ldg(P.l1 + b);
+    if (t >= nfull) {  // the partial last tile
+      general_tile<TIn, TC, kLut, 2>(P, t, slut, blockm ? l1v + run : ~0ull);
+      continue;
+    }
+    u32 pre = 0;
+    if (!blockm) {
+#pragma unroll
+      for (int r = 0; r < (TPL1 + 31) / 32; ++r) {
+        const u32 j = r * 32 + lane;
+        if (j < tb) pre += __ldg(P.tile_counts + b * TPL1 + j);
+      }
+#pragma unroll
+      for (int d = 16; d; d >>= 1) pre += __shfl_xor_sync(FULLM, pre, d);
+    }
+    const u64 P1 = l1v + (blockm ? run : pre);
+    const u64 t0 = (u64)t * TILE;
+    const u8* tin = ring + slot * TB;
+    w_mbar_wait(&mbar[slot], (it >> 1) & 1u);
+    // ---- one node? (first and last element of the tile) --------------------
+    u32 fkey, lkey;
+    {
+      const u32 f = sizeof(TIn) == 1 ? (u32)tin[0] : (u32)reinterpret_cast<const u16*>(tin)[0];
+      const u32 l = sizeof(TIn) == 1 ? (u32)tin[TILE - 1] : (u32)reinterpret_cast<const u16*>(tin)[TILE - 1];
+      const u32 fc = !kLut ? f : sizeof(TIn) == 1 ? (u32)slut[f] : (u32)__ldg(P.lut + f);
+      const u32 lc = !kLut ? l : sizeof(TIn) == 1 ? (u32)slut[l] : (u32)__ldg(P.lut + l);
+      fkey = fc >> P.shift_key;
+      lkey = lc >> P.shift_key;
+    }
+    if (fkey != lkey) {  // node boundary inside the tile: element by element
+      __syncwarp();
+      if (lane == 0 && tnext < nfull) w_load_tile(ring + slot * TB, in + (u64)tnext * TB, TB, &mbar[slot]);
+      run += general_tile<TIn, TC, kLut, 2>(P, t, slut, blockm ? l1v + run : ~0ull);
+      continue;
+    }
+    // ---- pass A: the lane's slice (chunk k = slice chunk k ^ (lane & 7)) ---
+    uint4 q[K];
+    u64 m[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) m[w] = 0;
+    const u8* src = tin + lane * (K * 16);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const u32 c = (u32)k ^ ((u32)lane & 7u);
+      q[k] = *reinterpret_cast<const uint4*>(src + c * 16);
+      wp_codes<TIn, TC>(q[k], slut, P.lut, kLut);
+      u32 mk = 0;
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2) {
+        u32 f0, f1;
+        wp_flags<TC>(q[k], s2, sh, f0, f1);
+        mk |= wp_gather(f0, f1) << (8 * s2);
+      }
+      const u32 bit = c * CE;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) m[w] |= (bit >> 6) == (u32)w ? (u64)mk << (bit & 63) : 0ull;
+    }
+    __syncwarp();
+    if (lane == 0 && tnext < nfull) w_load_tile(ring + slot * TB, in + (u64)tnext * TB, TB, &mbar[slot]);
+    u32 wc[NW], cl = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      wc[w] = __popcll(m[w]);
+      cl += wc[w];
+    }
+    u32 inc = cl;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 y = __shfl_up_sync(FULLM, inc, d);
+      if (lane >= d) inc += y;
+    }
+    const u32 tile_ones = __shfl_sync(FULLM, inc, 31);
+    const u32 pl = inc - cl;  // ones of the tile before this lane
+    run += tile_ones;
+    const u32 e0 = (u32)lane * E;
+    // ---- level l: words, L2 entries, select samples (rankselect.py:495-532)
+    {
+      u32 before = pl;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const u64 g = t0 + e0 + 64 * w;
+        P.words[g >> 6] = m[w];
+        if ((g & l2m) == 0) P.l2[g >> P.l2_log] = (u16)(P1 + before - l1v);
+        before += wc[w];
+      }
+#pragma unroll
+      for (int kind = 0; kind < 2; ++kind) {
+        const bool ones = kind == 0;
+        const u64 sb = ones ? P1 : t0 - P1;
+        const u32 cnt = ones ? tile_ones : TILE - tile_ones;
+        const u64 q0 = wnext_multiple(sb, P.rate, P.rate_log);
+        if (q0 > sb + cnt) continue;
+        const u32 lc = ones ? cl : E - cl;
+        const u32 lp = ones ? pl : e0 - pl;
+        u64* out = ones ? P.ones : P.zeros;
+        const u64 cap = ones ? P.ones_cap : P.zeros_cap;
+        for (u64 qo = q0; qo <= sb + cnt; qo += P.rate) {
+          u32 tt = (u32)(qo - sb);
+          if (lp < tt && tt <= lp + lc) {
+            tt -= lp;
+            u32 pos = e0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+              const u64 wm = ones ? m[w] : ~m[w];
+              const u32 pc = __popcll(wm);
+              if (tt > 0 && tt <= pc) {
+                pos = e0 + 64 * w + select_in_word64(wm, tt);
+                tt = 0;
+              } else if (tt > 0) {
+                tt -= pc;
+              }
+            }
+            const u64 sidx = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
+            if (sidx < cap) out[sidx] = t0 + pos;
+          }
+        }
+      }
+    }
+    // ---- the last level: the two group strings ------------------------------
+    const NodeEnt* ne = P.nodes + fkey;
+    const u64 zdst = (u64)__ldg(&ne->zero_base) + (t0 - P1);
+    const u64 odst = (u64)__ldg(&ne->one_base) + P1;
+    u32* gz = gbuf;
+    u32* go = gbuf + GW;
+    for (int i = lane; i < 2 * GW; i += 32) gbuf[i] = 0u;
+    __syncwarp();
+    const u32 zb = (u32)(zdst & 31) + (e0 - pl);  // this lane's first bit in each string
+    const u32 ob = (u32)(odst & 31) + pl;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const u32 c = (u32)k ^ ((u32)lane & 7u);
+      const u32 bit = c * CE;  // the chunk's first element in the slice
+      // ones of the slice before the chunk
+      u32 ob4 = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const u32 lo = (u32)w * 64;
+        const u64 mw = bit >= lo + 64 ? m[w] : bit <= lo ? 0ull : m[w] & ((1ull << (bit - lo)) - 1ull);
+        ob4 += __popcll(mw);
+      }
+      u32 pz = zb + (bit - ob4), po = ob + ob4;
+      u32 vz = 0, vo = 0, nz = 0, no = 0;  // the chunk's pieces (<= 16 bits)
+      {
+        const u64 mw = NW == 1 ? m[0] : ((bit >> 6) ? m[NW - 1] : m[0]);
+        const u32 mk = (u32)(mw >> (bit & 63)) & ((1u << CE) - 1u);
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2) {
+          const u32 m8 = (mk >> (8 * s2)) & 0xffu;
+          u32 f0, f1;
+          wp_flags<TC>(q[k], s2, sh1, f0, f1);
+          const uint2 so = csel[m8], sz = csel[~m8 & 0xffu];
+          const u32 go8 = wp_gather(__byte_perm(f0, f1, so.x), __byte_perm(f0, f1, so.y));
+          const u32 gz8 = wp_gather(__byte_perm(f0, f1, sz.x), __byte_perm(f0, f1, sz.y));
+          const u32 c1 = __popc(m8);
+          vo |= (go8 & ((1u << c1) - 1u)) << no;
+          vz |= (gz8 & ((0x100u >> c1) - 1u)) << nz;
+          no += c1;
+          nz += 8 - c1;
+        }
+      }
+      if (nz) {
+        atomicOr(gz + (pz >> 5), vz << (pz & 31));
+        if ((pz & 31) + nz > 32) atomicOr(gz + (pz >> 5) + 1, vz >> (32 - (pz & 31)));
+      }
+      if (no) {
+        atomicOr(go + (po >> 5), vo << (po & 31));
+        if ((po & 31) + no > 32) atomicOr(go + (po >> 5) + 1, vo >> (32 - (po & 31)));
+      }
+    }
+    __syncwarp();
+    // ---- write the group strings; the last level's ones per L1 block ------
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      const u64 dst = g ? odst : zdst;
+      const u32 cnt = g ? tile_ones : TILE - tile_ones;
+      if (!cnt) continue;
+      const u32* buf = g ? go : gz;
+      const u32 b0 = (u32)(dst & 31);
+      const u32 nwd = (b0 + cnt + 31) >> 5;
+      const u64 bnd = ((dst >> 16) + 1) << 16;
+      u32* nw32 = reinterpret_cast<u32*>(P.next_words) + (dst >> 5);
+      u32 lo = 0, hi = 0;
+      for (u32 w = lane; w < nwd; w += 32) {
+        const u32 v = buf[w];
+        const bool part = (w == 0 && b0) || (w == nwd - 1 && ((b0 + cnt) & 31));
+        if (part) {
+          if (v) atomicOr(nw32 + w, v);
+        } else {
+          nw32[w] = v;
+        }
+        // words straddle no L1 boundary (65536 is a multiple of 32)
+        if (((dst >> 5) + w) << 5 >= bnd) hi += __popc(v); else lo += __popc(v);
+      }
+      u32 x = lo | (hi << 16);
+#pragma unroll
+      for (int d = 16; d; d >>= 1) x += __shfl_xor_sync(FULLM, x, d);
+      if (lane == 0 && (x & 0xffffu)) atomicAdd(P.next_l1_counts + (dst >> 16), x & 0xffffu);
+      if (lane == 1 && (x >> 16)) atomicAdd(P.next_l1_counts + (bnd >> 16), x >> 16);
+    }
+    __syncwarp();  // the strings are re-zeroed by the next tile
+  }
+}
+
+// ---------------------------------------------------------------------------
 // level 0: ones per warp tile of the text's top code bit (streaming pass)
 // ---------------------------------------------------------------------------
 // Codes are monotone in the symbol (the minimal alphabet and the reduced-tree
@@ -1481,9 +1824,41 @@ __global__ void __launch_bounds__(D_NT) dir_kernel(const __grid_constant__ DirPa
 }
 
 namespace {
+// pair kernel launch (MODE 2): 8 warps per CTA, per-warp ring + group strings
+template <typename TIn, typename TC, bool kLut>
+cudaError_t launch_pair(const WLevelParams& p, int sms, cudaStream_t st) {
+  constexpr int GW = WS<TIn>::TILE / 32 + 2;
+  const int smem = 8 * (2 * WS<TIn>::BYTES + 16 + 2 * GW * 4);
+  auto kern = wpair_kernel<TIn, TC, kLut>;
+  static std::atomic<int> cached[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const bool dev_ok = dev >= 0 && dev < 64;
+  int per_sm = dev_ok ? cached[dev].load(std::memory_order_acquire) : 0;
+  if (per_sm <= 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+    if (per_sm < 1) per_sm = 1;
+    if (dev_ok) cached[dev].store(per_sm, std::memory_order_release);
+  }
+  const u64 tiles = (p.m + WS<TIn>::TILE - 1) / WS<TIn>::TILE;
+  const u64 units = p.tile_counts ? tiles : (tiles + WS<TIn>::TPL1 - 1) / WS<TIn>::TPL1;
+  const u64 need = (units + 7) / 8;
+  const u64 cap = (u64)sms * per_sm;
+  kern<<<(unsigned)(need < cap ? need : cap), 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
 template <typename TIn, typename TC, bool kLut, int MODE>
 cudaError_t launch_w(const WLevelParams& p, int sms, cudaStream_t st) {
   constexpr bool kPair = MODE == 2;
+  // the pair kernel handles u8 codes from either input and u16 codes from u16 input
+  if (kPair && !(sizeof(TIn) == 2 && sizeof(TC) == 1 && !kLut) && !(sizeof(TIn) == 1 && sizeof(TC) == 2)) {
+    const char* e = getenv("WT_PAIR_KERNEL");  // "stage": the staging variant (A/B)
+    if (!(e && e[0] == 's')) return launch_pair<TIn, TC, kLut>(p, sms, st);
+  }
   const size_t smem = 512 + (size_t)W_WARPS * WF<TIn, TC>::WARP_SMEM;
   auto kern = wlevel_kernel<TIn, TC, kLut, MODE>;
   // attribute + occupancy once per device (host cost off the per-level path)

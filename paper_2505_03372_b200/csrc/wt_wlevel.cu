@@ -869,6 +869,35 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? W_MINB4 : W_MINB
       zc = t - oc;
     }
     u32 r1[ROWS], rtot[ROWS];
+    // four rows per warp scan, 8-bit fields: a lane-row holds <= 8 ones, so
+    // every lane's inclusive field stays <= 248 except lane 31's (<= 256,
+    // which may carry): the exclusive prefixes are read from lane - 1 and the
+    // row totals are lane 31's exclusive prefix plus its own counts
+    static_assert(ROWS % 4 == 0, "rows come in fours");
+#ifndef WT_SCAN4
+#define WT_SCAN4 1
+#endif
+#if WT_SCAN4
+#pragma unroll
+    for (int r = 0; r < ROWS; r += 4) {
+      const u32 x = (u32)__popc(mrow[r]) | ((u32)__popc(mrow[r + 1]) << 8) |
+                    ((u32)__popc(mrow[r + 2]) << 16) | ((u32)__popc(mrow[r + 3]) << 24);
+      u32 inc = x;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u32 y = __shfl_up_sync(FULLM, inc, d);
+        if (lane >= d) inc += y;
+      }
+      u32 ex = __shfl_up_sync(FULLM, inc, 1);
+      if (lane == 0) ex = 0;
+      const u32 ex31 = __shfl_sync(FULLM, ex, 31), x31 = __shfl_sync(FULLM, x, 31);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        r1[r + i] = (ex >> (8 * i)) & 0xffu;
+        rtot[r + i] = ((ex31 >> (8 * i)) & 0xffu) + ((x31 >> (8 * i)) & 0xffu);
+      }
+    }
+#else
 #pragma unroll
     for (int r = 0; r < ROWS; r += 2) {
       const u32 x = (u32)__popc(mrow[r]) | ((u32)__popc(mrow[r + 1]) << 16);
@@ -885,6 +914,7 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? W_MINB4 : W_MINB
       rtot[r] = tot & 0xffffu;
       rtot[r + 1] = tot >> 16;
     }
+#endif
     u32 tile_ones = 0;
     u32 rstart[ROWS];  // ones of the tile before row r (warp-uniform)
 #pragma unroll
@@ -1348,20 +1378,23 @@ template <typename TIn, typename TC>
 __device__ __forceinline__ void wp_codes(uint4& q, const u16* slut, const u16* glut, bool lut) {
   // 16 input bytes -> 16 code bytes (u8 codes) or 8 code halfwords (u16)
   if (!lut) return;
-  const u32 w[4] = {q.x, q.y, q.z, q.w};
-  u32 o[4] = {0, 0, 0, 0};
   if (sizeof(TIn) == 1) {  // u8 text, u8 codes (L = 2 here)
-#pragma unroll
-    for (int j = 0; j < 16; ++j) o[j >> 2] |= (u32)slut[(w[j >> 2] >> ((j & 3) * 8)) & 0xffu] << ((j & 3) * 8);
-    q = make_uint4(o[0], o[1], o[2], o[3]);
-  } else if (sizeof(TC) == 1) {  // u16 text, u8 codes: 8 codes in the low 8 bytes
-#pragma unroll
-    for (int j = 0; j < 8; ++j) o[j >> 2] |= (u32)__ldg(glut + ((w[j >> 1] >> ((j & 1) * 16)) & 0xffffu)) << ((j & 3) * 8);
-    q = make_uint4(o[0], o[1], 0u, 0u);
+    auto map4 = [&](u32 x) -> u32 {
+      return (u32)slut[x & 0xffu] | ((u32)slut[(x >> 8) & 0xffu] << 8) |
+             ((u32)slut[(x >> 16) & 0xffu] << 16) | ((u32)slut[x >> 24] << 24);
+    };
+    q = make_uint4(map4(q.x), map4(q.y), map4(q.z), map4(q.w));
   } else {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) o[j >> 1] |= (u32)__ldg(glut + ((w[j >> 1] >> ((j & 1) * 16)) & 0xffffu)) << ((j & 1) * 16);
-    q = make_uint4(o[0], o[1], o[2], o[3]);
+    auto g = [&](u32 x) -> u32 { return (u32)__ldg(glut + x); };
+    if (sizeof(TC) == 1) {  // u16 text, u8 codes: 8 codes in the low 8 bytes
+      auto map4 = [&](u32 x, u32 y) -> u32 {
+        return g(x & 0xffffu) | (g(x >> 16) << 8) | (g(y & 0xffffu) << 16) | (g(y >> 16) << 24);
+      };
+      q = make_uint4(map4(q.x, q.y), map4(q.z, q.w), 0u, 0u);
+    } else {
+      auto map2 = [&](u32 x) -> u32 { return g(x & 0xffffu) | (g(x >> 16) << 16); };
+      q = make_uint4(map2(q.x), map2(q.y), map2(q.z), map2(q.w));
+    }
   }
 }
 
@@ -1395,21 +1428,20 @@ __global__ void __launch_bounds__(256, 2) wpair_kernel(const __grid_constant__ W
   constexpr int E = K * CE;                  // elements per lane (128 | 64)
   constexpr int NW = E / 64;                 // level-l words per lane (2 | 1)
   constexpr int NS = CE / 8;                 // 8-element steps per chunk (2 | 1)
-  constexpr int GW = TILE / 32 + 2;          // words of one group string (+ alignment)
+  constexpr int GW = TILE / 32 + 4;          // words of one group string (+ alignment; 2 GW % 4 == 0)
   static_assert(K == 8, "chunk rotation assumes 8 chunks per lane");
-  // PRMT selectors compacting the bytes of an 8-element step whose mask bit
-  // is set: selector nibble i = source byte of output byte i
+  // sheep-and-goats PRMT selectors of an 8-element step: output bytes = the
+  // bytes whose mask bit is 0, in order, then those whose bit is 1 (selector
+  // nibble i = source byte of output byte i)
   __shared__ uint2 csel[256];
   __shared__ u16 slut[kLut && sizeof(TIn) == 1 ? 256 : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   {
-    u32 lo = 0, hi = 0, n = 0;
-    for (u32 j = 0; j < 8; ++j)
-      if ((tid >> j) & 1) {
-        if (n < 4) lo |= j << (4 * n); else hi |= j << (4 * (n - 4));
-        ++n;
-      }
-    csel[tid] = make_uint2(lo, hi);
+    u32 sel = 0, n = 0;
+    for (u32 pass = 0; pass < 2; ++pass)
+      for (u32 j = 0; j < 8; ++j)
+        if (((tid >> j) & 1) == pass) sel |= j << (4 * n++);
+    csel[tid] = make_uint2(sel & 0xffffu, sel >> 16);
     if (kLut && sizeof(TIn) == 1) slut[tid] = P.lut[tid];
     __syncthreads();
   }
@@ -1567,42 +1599,50 @@ __global__ void __launch_bounds__(256, 2) wpair_kernel(const __grid_constant__ W
     const u64 odst = (u64)__ldg(&ne->one_base) + P1;
     u32* gz = gbuf;
     u32* go = gbuf + GW;
-    for (int i = lane; i < 2 * GW; i += 32) gbuf[i] = 0u;
+    for (int i = lane; i < GW / 2; i += 32) reinterpret_cast<uint4*>(gbuf)[i] = make_uint4(0, 0, 0, 0);
     __syncwarp();
     const u32 zb = (u32)(zdst & 31) + (e0 - pl);  // this lane's first bit in each string
     const u32 ob = (u32)(odst & 31) + pl;
+    // chunks k and k + 1 are slice chunks c and c ^ 1: an adjacent pair, one
+    // piece of <= 32 bits per group
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < K; k += 2) {
       const u32 c = (u32)k ^ ((u32)lane & 7u);
-      const u32 bit = c * CE;  // the chunk's first element in the slice
-      // ones of the slice before the chunk
-      u32 ob4 = 0;
+      const u32 ce = c & ~1u;  // the pair's even chunk (first in the slice)
+      const u32 bit = ce * CE;
+      u32 ob4 = 0;  // ones of the slice before the pair
 #pragma unroll
       for (int w = 0; w < NW; ++w) {
         const u32 lo = (u32)w * 64;
         const u64 mw = bit >= lo + 64 ? m[w] : bit <= lo ? 0ull : m[w] & ((1ull << (bit - lo)) - 1ull);
         ob4 += __popcll(mw);
       }
-      u32 pz = zb + (bit - ob4), po = ob + ob4;
-      u32 vz = 0, vo = 0, nz = 0, no = 0;  // the chunk's pieces (<= 16 bits)
-      {
-        const u64 mw = NW == 1 ? m[0] : ((bit >> 6) ? m[NW - 1] : m[0]);
-        const u32 mk = (u32)(mw >> (bit & 63)) & ((1u << CE) - 1u);
+      u32 vz = 0, vo = 0, nz = 0, no = 0;
+      // c & 1 == lane & 1 (k is even): odd lanes hold the pair's even chunk in q[k + 1]
+      const bool odd = (lane & 1) != 0;
+      uint4 qp[2];
+      qp[0] = odd ? q[k + 1] : q[k];
+      qp[1] = odd ? q[k] : q[k + 1];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // even chunk first
+        const u32 cb = (ce + h) * CE;
+        const u64 mw = NW == 1 ? m[0] : ((cb >> 6) ? m[NW - 1] : m[0]);
+        const u32 mk = (u32)(mw >> (cb & 63)) & ((1u << CE) - 1u);
 #pragma unroll
         for (int s2 = 0; s2 < NS; ++s2) {
           const u32 m8 = (mk >> (8 * s2)) & 0xffu;
           u32 f0, f1;
-          wp_flags<TC>(q[k], s2, sh1, f0, f1);
-          const uint2 so = csel[m8], sz = csel[~m8 & 0xffu];
-          const u32 go8 = wp_gather(__byte_perm(f0, f1, so.x), __byte_perm(f0, f1, so.y));
-          const u32 gz8 = wp_gather(__byte_perm(f0, f1, sz.x), __byte_perm(f0, f1, sz.y));
-          const u32 c1 = __popc(m8);
-          vo |= (go8 & ((1u << c1) - 1u)) << no;
-          vz |= (gz8 & ((0x100u >> c1) - 1u)) << nz;
+          wp_flags<TC>(qp[h], s2, sh1, f0, f1);
+          const uint2 sg = csel[m8];
+          const u32 v8 = wp_gather(__byte_perm(f0, f1, sg.x), __byte_perm(f0, f1, sg.y));
+          const u32 c1 = __popc(m8), c0 = 8 - c1;
+          vz |= (v8 & ((1u << c0) - 1u)) << nz;
+          vo |= (v8 >> c0) << no;
+          nz += c0;
           no += c1;
-          nz += 8 - c1;
         }
       }
+      const u32 pz = zb + (bit - ob4), po = ob + ob4;
       if (nz) {
         atomicOr(gz + (pz >> 5), vz << (pz & 31));
         if ((pz & 31) + nz > 32) atomicOr(gz + (pz >> 5) + 1, vz >> (32 - (pz & 31)));
@@ -1620,27 +1660,25 @@ __global__ void __launch_bounds__(256, 2) wpair_kernel(const __grid_constant__ W
       const u32 cnt = g ? tile_ones : TILE - tile_ones;
       if (!cnt) continue;
       const u32* buf = g ? go : gz;
-      const u32 b0 = (u32)(dst & 31);
-      const u32 nwd = (b0 + cnt + 31) >> 5;
-      const u64 bnd = ((dst >> 16) + 1) << 16;
+      const u32 b0 = (u32)(dst & 31), e = b0 + cnt;
+      const u32 nwd = (e + 31) >> 5;
+      // the first word of the next L1 block, relative to the string's first word
+      const u32 wsplit = (u32)(((((dst >> 16) + 1) << 16) - (dst & ~31ull)) >> 5);
       u32* nw32 = reinterpret_cast<u32*>(P.next_words) + (dst >> 5);
-      u32 lo = 0, hi = 0;
+      u32 x = 0;  // ones before the split | after << 16
       for (u32 w = lane; w < nwd; w += 32) {
         const u32 v = buf[w];
-        const bool part = (w == 0 && b0) || (w == nwd - 1 && ((b0 + cnt) & 31));
-        if (part) {
+        if ((w == 0 && b0) || (w == nwd - 1 && (e & 31))) {
           if (v) atomicOr(nw32 + w, v);
         } else {
           nw32[w] = v;
         }
-        // words straddle no L1 boundary (65536 is a multiple of 32)
-        if (((dst >> 5) + w) << 5 >= bnd) hi += __popc(v); else lo += __popc(v);
+        x += (u32)__popc(v) << (w >= wsplit ? 16 : 0);
       }
-      u32 x = lo | (hi << 16);
 #pragma unroll
       for (int d = 16; d; d >>= 1) x += __shfl_xor_sync(FULLM, x, d);
       if (lane == 0 && (x & 0xffffu)) atomicAdd(P.next_l1_counts + (dst >> 16), x & 0xffffu);
-      if (lane == 1 && (x >> 16)) atomicAdd(P.next_l1_counts + (bnd >> 16), x >> 16);
+      if (lane == 1 && (x >> 16)) atomicAdd(P.next_l1_counts + (dst >> 16) + 1, x >> 16);
     }
     __syncwarp();  // the strings are re-zeroed by the next tile
   }
@@ -1766,59 +1804,102 @@ __global__ void __launch_bounds__(1024) l1_scan_kernel(const u32* __restrict__ c
 }
 
 // L2 entries and select samples of a level from its bit-vector and L1
-// directory (rankselect.py:495-532; the level a pair-mode launch wrote): one
-// warp per 65536-bit L1 block, 64 words per step (one 16-byte load per lane),
-// a warp scan of the word-pair popcounts gives every L2 prefix.
+// directory (rankselect.py:495-532): one warp per 65536-bit L1 block, 128
+// words per step (four per lane, two 16-byte loads), a warp scan of the
+// lanes' popcounts gives every L2 prefix.  Offsets inside the block are
+// 32-bit; a lane looks for samples only when an ordinal multiple of the
+// rate falls in its range (about one lane in 16 per step at rate 4096).
 constexpr int D_NT = 256;
+__device__ __noinline__ void dir_samples(const DirParams& P, u64 ob, u64 zb, u64 w0, const u64 (&w)[4],
+                                         u32 valid) {
+  // ones: ordinals (ob, ob + c], zeros: (zb, zb + zc] over the lane's words
+#pragma unroll
+  for (int kind = 0; kind < 2; ++kind) {
+    const bool ones = kind == 0;
+    u64 wm[4];
+    u32 cw[4], tot = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const u32 vb = valid > 64u * j ? min(64u, valid - 64u * j) : 0u;
+      const u64 vm = vb >= 64 ? ~0ull : (1ull << vb) - 1ull;
+      wm[j] = (ones ? w[j] : ~w[j]) & vm;
+      cw[j] = __popcll(wm[j]);
+      tot += cw[j];
+    }
+    const u64 base = ones ? ob : zb;
+    u64* out = ones ? P.ones : P.zeros;
+    const u64 cap = ones ? P.ones_cap : P.zeros_cap;
+    for (u64 qo = wnext_multiple(base, P.rate, P.rate_log); qo <= base + tot; qo += P.rate) {
+      u32 k = (u32)(qo - base);
+      u64 pos = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (k > 0 && k <= cw[j]) {
+          pos = ((w0 + j) << 6) + select_in_word64(wm[j], k);
+          k = 0;
+        } else if (k > 0) {
+          k -= cw[j];
+        }
+      }
+      const u64 si = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
+      if (si < cap) out[si] = pos;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(D_NT) dir_kernel(const __grid_constant__ DirParams P) {
   const int lane = threadIdx.x & 31;
   const u64 nw = (P.m + 63) >> 6;
   const u64 nblk = (P.m + kL1Bits - 1) / kL1Bits;
-  const u64 l2w = ((1ull << P.l2_log) >> 6) - 1;  // L2 block = l2w + 1 words
+  const u32 l2w = (u32)((1ull << P.l2_log) >> 6) - 1u;  // L2 block = l2w + 1 words
+  const bool pow2 = P.rate_log >= 0;
   for (u64 b = (u64)blockIdx.x * (D_NT / 32) + (threadIdx.x >> 5); b < nblk;
        b += (u64)gridDim.x * (D_NT / 32)) {
     const u64 l1v = __ldg(P.l1 + b);
+    const u64 bw = b * (kL1Bits / 64);  // the block's first word
+    const u32 nbw = (u32)min((u64)(kL1Bits / 64), nw - bw);
     u32 carry = 0;  // ones of the block before this step
-    for (u64 s = b * (kL1Bits / 64); s < (b + 1) * (kL1Bits / 64) && s < nw; s += 64) {
-      const u64 wi = s + 2 * (u64)lane;
-      ulonglong2 v = make_ulonglong2(0ull, 0ull);
-      if (wi + 1 < nw)
-        v = __ldg(reinterpret_cast<const ulonglong2*>(P.words + wi));
-      else if (wi < nw)
-        v.x = __ldg(P.words + wi);
-      const u32 c0 = __popcll(v.x), c = c0 + __popcll(v.y);
+    for (u32 s = 0; s < nbw; s += 128) {
+      const u32 lw = s + 4 * (u32)lane;  // the lane's first word in the block
+      u64 w[4] = {0ull, 0ull, 0ull, 0ull};
+      if (lw + 4 <= nbw) {
+        const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(P.words + bw + lw));
+        const ulonglong2 c2 = __ldg(reinterpret_cast<const ulonglong2*>(P.words + bw + lw) + 1);
+        w[0] = a.x; w[1] = a.y; w[2] = c2.x; w[3] = c2.y;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (lw + j < nbw) w[j] = __ldg(P.words + bw + lw + j);
+      }
+      u32 pc[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) pc[j] = __popcll(w[j]);
+      const u32 c = pc[0] + pc[1] + pc[2] + pc[3];
       u32 inc = c;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const u32 y = __shfl_up_sync(FULLM, inc, d);
         if (lane >= d) inc += y;
       }
-      const u32 ex = carry + inc - c;  // ones of the block before word wi
+      const u32 ex = carry + inc - c;  // ones of the block before word lw
       carry += __shfl_sync(FULLM, inc, 31);
-      if (wi >= nw) continue;
-      if ((wi & l2w) == 0) P.l2[(wi << 6) >> P.l2_log] = (u16)ex;
-      if (wi + 1 < nw && ((wi + 1) & l2w) == 0) P.l2[((wi + 1) << 6) >> P.l2_log] = (u16)(ex + c0);
-      // select samples: every rate-th one / zero (1-based ordinals)
-      const u64 ob = l1v + ex;
-      for (u64 qo = wnext_multiple(ob, P.rate, P.rate_log); qo <= ob + c; qo += P.rate) {
-        const u32 k = (u32)(qo - ob);
-        const u64 pos = k <= c0 ? (wi << 6) + select_in_word64(v.x, k)
-                                : ((wi + 1) << 6) + select_in_word64(v.y, k - c0);
-        const u64 si = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
-        if (si < P.ones_cap) P.ones[si] = pos;
+      if (lw >= nbw) continue;
+      u32 pre = ex;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (lw + j < nbw && ((lw + j) & l2w) == 0)
+          P.l2[((bw + lw + j) << 6) >> P.l2_log] = (u16)pre;
+        pre += pc[j];
       }
-      const u64 valid = min((u64)128, P.m - (wi << 6));
-      const u64 zb = (wi << 6) - ob;
-      const u64 zm0 = ~v.x & (valid >= 64 ? ~0ull : (1ull << valid) - 1);
-      const u64 zm1 = valid <= 64 ? 0ull : ~v.y & (valid >= 128 ? ~0ull : (1ull << (valid - 64)) - 1);
-      const u32 z0 = __popcll(zm0), zc = z0 + __popcll(zm1);
-      for (u64 qo = wnext_multiple(zb, P.rate, P.rate_log); qo <= zb + zc; qo += P.rate) {
-        const u32 k = (u32)(qo - zb);
-        const u64 pos = k <= z0 ? (wi << 6) + select_in_word64(zm0, k)
-                                : ((wi + 1) << 6) + select_in_word64(zm1, k - z0);
-        const u64 si = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
-        if (si < P.zeros_cap) P.zeros[si] = pos;
-      }
+      // samples: only when a multiple of the rate falls in the lane's range
+      const u64 g0 = (bw + lw) << 6;  // the lane's first bit
+      const u32 valid = (u32)min((u64)256, P.m - g0);
+      const u64 ob = l1v + ex, zb = g0 - ob;
+      const u32 zc = valid - c;
+      const bool hit = pow2 ? (((ob + c) >> P.rate_log) != (ob >> P.rate_log)) ||
+                                  (((zb + zc) >> P.rate_log) != (zb >> P.rate_log))
+                            : ((ob + c) / P.rate != ob / P.rate) || ((zb + zc) / P.rate != zb / P.rate);
+      if (hit) dir_samples(P, ob, zb, bw + lw, w, valid);
     }
   }
 }
@@ -1827,7 +1908,7 @@ namespace {
 // pair kernel launch (MODE 2): 8 warps per CTA, per-warp ring + group strings
 template <typename TIn, typename TC, bool kLut>
 cudaError_t launch_pair(const WLevelParams& p, int sms, cudaStream_t st) {
-  constexpr int GW = WS<TIn>::TILE / 32 + 2;
+  constexpr int GW = WS<TIn>::TILE / 32 + 4;
   const int smem = 8 * (2 * WS<TIn>::BYTES + 16 + 2 * GW * 4);
   auto kern = wpair_kernel<TIn, TC, kLut>;
   static std::atomic<int> cached[64];

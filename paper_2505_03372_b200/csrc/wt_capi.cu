@@ -372,11 +372,13 @@ static int alloc_tree(wt_tree* t, cudaStream_t st) {
 }
 
 // query-side layout of every level; totals_dev[l] = ones of level l (device)
-static int launch_qlayouts(wt_tree* t, const u64* totals_dev, cudaStream_t st) {
+static int launch_qlayouts(wt_tree* t, const u64* totals_dev, cudaStream_t st,
+                           const std::vector<char>* done = nullptr) {
   const Plan& P = t->plan;
   uint32_t sh = 0;
   while ((1u << sh) < t->meta.l2_bits) ++sh;
   for (uint32_t l = 0; l < P.L; ++l) {
+    if (done && l < done->size() && (*done)[l]) continue;  // written by dirq_kernel
     LevelHost& h = t->lv[l];
     LevelDev d{};
     d.words = t->words + (P.offsets[l] >> 6);
@@ -646,6 +648,7 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       TRY(S.get(&p, (uint64_t)P.sizes[2] * P.code_bytes + 16));
       cur[1] = p;
     }
+    std::vector<char> q_done(P.L, 0);  // levels whose query layout dirq_kernel wrote
     {
       // K2w: warp tiles; per-tile and per-L1-block ones counts of each level
       // come from the previous level's scatter (level 0: a counting pass)
@@ -706,7 +709,45 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       const char* pe = getenv("WT_PAIR");
       const bool pair_ok = !(pe && pe[0] == '0');
       const char* de = getenv("WT_DIR");
-      const bool dir_after = !(de && de[0] == '0');
+      const char* qe = getenv("WT_DIRQ");
+      // After each partitioning level's kernel, dir_kernel writes its L2
+      // entries + select samples (a streaming pass over its bits; WT_DIR=0:
+      // inside the level kernel); WT_DIRQ=1: dirq_kernel writes them together
+      // with the level's query lines (measured slower: latency bound)
+      const bool dirq_on = qe && qe[0] == '1';
+      const bool dir_after = dirq_on || !(de && de[0] == '0');
+      auto level_dir = [&](uint32_t lv, const u64* words) -> int {
+        LevelHost& hl = t->lv[lv];
+        const uint64_t mm = hl.meta.n_bits;
+        DirParams dp{};
+        dp.words = words;
+        dp.m = mm;
+        dp.l1 = hl.l1;
+        dp.l2 = hl.l2;
+        dp.ones = hl.ones;
+        dp.zeros = hl.zeros;
+        dp.ones_cap = mm / sample_rate;
+        dp.zeros_cap = mm / sample_rate;
+        dp.l2_log = l2_log;
+        dp.rate_log = rate_log_of(sample_rate);
+        dp.rate = sample_rate;
+        if (!dirq_on) {
+          CU(launch_dir(dp, sm_count(device), st));
+          return WT_OK;
+        }
+        DirQParams q{};
+        q.d = dp;
+        q.total = totals + lv;
+        q.lines = hl.lines;
+        q.n_lines = hl.n_lines;
+        q.sel1 = hl.sel1;
+        q.sel0 = hl.sel0;
+        q.cap1 = hl.sel_cap;
+        q.cap0 = hl.sel_cap;
+        CU(launch_dirq(q, sm_count(device), st));
+        q_done[lv] = 1;
+        return WT_OK;
+      };
       int ci = 0;
       for (uint32_t l = 0; l < P.L; ++l) {
         const uint64_t m = (uint64_t)P.sizes[l];
@@ -760,46 +801,20 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
         // kernel (WT_DIR=0: inside)
         wp.skip_dir = dir_after && wp.out ? 1 : 0;
         CU(launch_wlevel(wp, in_bytes, P.code_bytes, l == 0 && dlut != nullptr, sm_count(device), st));
-        if (wp.skip_dir) {
-          DirParams dp{};
-          dp.words = wp.words;
-          dp.m = m;
-          dp.l1 = h.l1;
-          dp.l2 = h.l2;
-          dp.ones = h.ones;
-          dp.zeros = h.zeros;
-          dp.ones_cap = m / sample_rate;
-          dp.zeros_cap = m / sample_rate;
-          dp.l2_log = l2_log;
-          dp.rate_log = rate_log_of(sample_rate);
-          dp.rate = sample_rate;
-          CU(launch_dir(dp, sm_count(device), st));
-        }
+        if (wp.skip_dir || (dirq_on && wp.m)) TRY(level_dir(l, wp.words));
         ci ^= 1;
         if (pair) {  // the last level: L1 from the pair pass's counts, then L2 + samples
           LevelHost& hn = t->lv[l + 1];
           CU(cudaEventRecord(lev[l + 1], st));
           CU(launch_l1_scan(l1cnt[ci], hn.meta.n_l1, hn.l1, totals + l + 1, st));
-          DirParams dp{};
-          dp.words = wp.next_words;
-          dp.m = wp.m_next;
-          dp.l1 = hn.l1;
-          dp.l2 = hn.l2;
-          dp.ones = hn.ones;
-          dp.zeros = hn.zeros;
-          dp.ones_cap = wp.m_next / sample_rate;
-          dp.zeros_cap = wp.m_next / sample_rate;
-          dp.l2_log = l2_log;
-          dp.rate_log = rate_log_of(sample_rate);
-          dp.rate = sample_rate;
-          CU(launch_dir(dp, sm_count(device), st));
+          TRY(level_dir(l + 1, wp.next_words));
           break;
         }
       }
       // (the query-side layouts run after the last level: overlapping them
       // with the next level's kernel on a side stream measured slower)
     }
-    TRY(launch_qlayouts(t, totals, st));
+    TRY(launch_qlayouts(t, totals, st, &q_done));
     tr.mark("levels launched");
     if (P.L) CU(cudaEventRecord(lev[P.L], st));
     CU(cudaEventRecord(e1, st));

@@ -106,6 +106,19 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
 
 // query-side rank-line layout (wt_qlayout.cu)
 u64 qlayout_lines(u64 n_bits);
+// one streaming pass over a level whose bits and L1 directory exist: its L2
+// entries and select samples (the reference directory) AND its query lines
+// with their line samples (wt_qlayout.cu); replaces dir_kernel + qlayout
+struct DirQParams {
+  DirParams d;
+  const u64* total;  // the level's ones (device)
+  ulonglong2* lines;
+  u64 n_lines;
+  u32* sel1;
+  u32* sel0;
+  u64 cap1, cap0;
+};
+cudaError_t launch_dirq(const DirQParams& p, int sms, cudaStream_t st);
 cudaError_t launch_qlayout(const LevelDev& L, const u64* total, u32 l2_shift, ulonglong2* lines,
                            u64 n_lines, u32* sel1, u64 cap1, u32* sel0, u64 cap0, cudaStream_t st);
 

@@ -57,6 +57,9 @@ constexpr int W_MINB = WT_W_MINB;  // __launch_bounds__ min CTAs per SM
 #define WT_W_MINB4 4
 #endif
 constexpr int W_MINB4 = WT_W_MINB4;  // the same for 4 KiB tiles (u8 input)
+#ifndef WT_SAG
+#define WT_SAG 0  // u8 levels: sheep-and-goats permutation scatter (measured slower than the cursors)
+#endif
 constexpr unsigned FULLM = 0xffffffffu;
 
 // a warp tile is 2048 elements for both input widths (2 KiB of u8 / 4 KiB
@@ -684,6 +687,20 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? W_MINB4 : W_MINB
     }
     __syncthreads();
   }
+  // u8 codes: sheep-and-goats PRMT selectors per 8-bit lane-row mask (zeros'
+  // bytes first, then ones', each in order; nibble i = source byte of output i)
+  constexpr bool kSag = sizeof(TC) == 1 && sizeof(TIn) == 1 && !kLut && WT_SAG;
+  __shared__ uint2 ssag[kSag ? 256 : 1];
+  if (kSag) {
+    for (int i = tid; i < 256; i += W_NT) {
+      u32 sel = 0, n = 0;
+      for (u32 pass = 0; pass < 2; ++pass)
+        for (u32 j = 0; j < 8; ++j)
+          if ((((u32)i >> j) & 1u) == pass) sel |= j << (4 * n++);
+      ssag[i] = make_uint2(sel & 0xffffu, sel >> 16);
+    }
+    __syncthreads();
+  }
   const u32 ntiles = (u32)((P.m + TILE - 1) / TILE);
   const u32 nfull = (u32)(P.m / TILE);
   const u32 gw = blockIdx.x * W_WARPS + warp, nw = gridDim.x * W_WARPS;
@@ -1055,6 +1072,22 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? W_MINB4 : W_MINB
           const u32 m = mrow[r];
           u32 oa = sbase + ooff + r1[r] * SZ;
           u32 za = sbase + zoff + ((u32)(r * RE + lane * CR) - r1[r]) * SZ;
+          if (kSag) {
+            // u8 codes: one sheep-and-goats byte permutation puts the row's
+            // zeros first and its ones after them (both in order); output byte
+            // k then goes to za + k (k < zeros) or oa - zeros + k -- no cursor
+            // updates, one store per element
+            const uint2 sg = ssag[m];
+            const u32 p0 = __byte_perm(cw[0], cw[WR - 1], sg.x), p1 = __byte_perm(cw[0], cw[WR - 1], sg.y);
+            const u32 nz = 8u - (u32)__popc(m);
+            const u32 bo = oa - nz;
+            const u32 therm = (1u << nz) - 1u;  // bit k: output byte k is a zero's
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const u32 val = (k < 4 ? p0 : p1) >> ((k & 3) * 8);
+              st_shared<TC>(((therm >> k) & 1u ? za : bo) + k, val);
+            }
+          } else {
 #pragma unroll
           for (int j = 0; j < CR; ++j) {
             // st.shared.u8/u16 keep the low bits: no masking of the element
@@ -1067,6 +1100,7 @@ __global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? W_MINB4 : W_MINB
               st_shared<TC>(za, val);
               za += SZ;
             }
+          }
           }
         }
       } else {  // two nodes: four runs
@@ -1804,102 +1838,99 @@ __global__ void __launch_bounds__(1024) l1_scan_kernel(const u32* __restrict__ c
 }
 
 // L2 entries and select samples of a level from its bit-vector and L1
-// directory (rankselect.py:495-532): one warp per 65536-bit L1 block, 128
-// words per step (four per lane, two 16-byte loads), a warp scan of the
-// lanes' popcounts gives every L2 prefix.  Offsets inside the block are
-// 32-bit; a lane looks for samples only when an ordinal multiple of the
-// rate falls in its range (about one lane in 16 per step at rate 4096).
-constexpr int D_NT = 256;
-__device__ __noinline__ void dir_samples(const DirParams& P, u64 ob, u64 zb, u64 w0, const u64 (&w)[4],
-                                         u32 valid) {
-  // ones: ordinals (ob, ob + c], zeros: (zb, zb + zc] over the lane's words
+// directory (rankselect.py:495-532): one 128-thread CTA per 65536-bit L1
+// block, thread i owns words [8 i, 8 i + 8) (four 16-byte loads), a CTA scan
+// of the threads' popcounts gives every L2 prefix; a thread selects only when
+// an ordinal multiple of the rate falls in its 512 bits (~1 in 8 threads at
+// rate 4096).  Full occupancy keeps enough loads in flight.
+// the select samples of one dir_kernel thread's 512 bits (rare: reloads its
+// words from L1 / L2, so the hot path keeps nothing live for it)
+__device__ __noinline__ void dir_hit(const DirParams& P, u64 w0, u64 nw, u32 valid, u64 ob, u64 zb,
+                                     u32 c, u32 zc) {
+  u64 w[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) w[j] = w0 + j < nw ? __ldg(P.words + w0 + j) : 0ull;
 #pragma unroll
   for (int kind = 0; kind < 2; ++kind) {
     const bool ones = kind == 0;
-    u64 wm[4];
-    u32 cw[4], tot = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const u32 vb = valid > 64u * j ? min(64u, valid - 64u * j) : 0u;
-      const u64 vm = vb >= 64 ? ~0ull : (1ull << vb) - 1ull;
-      wm[j] = (ones ? w[j] : ~w[j]) & vm;
-      cw[j] = __popcll(wm[j]);
-      tot += cw[j];
-    }
     const u64 base = ones ? ob : zb;
-    u64* out = ones ? P.ones : P.zeros;
-    const u64 cap = ones ? P.ones_cap : P.zeros_cap;
-    for (u64 qo = wnext_multiple(base, P.rate, P.rate_log); qo <= base + tot; qo += P.rate) {
+    const u32 cnt = ones ? c : zc;
+    for (u64 qo = wnext_multiple(base, P.rate, P.rate_log); qo <= base + cnt; qo += P.rate) {
       u32 k = (u32)(qo - base);
       u64 pos = 0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (k > 0 && k <= cw[j]) {
-          pos = ((w0 + j) << 6) + select_in_word64(wm[j], k);
+      for (int j = 0; j < 8; ++j) {
+        const u32 vb = valid > 64u * j ? min(64u, valid - 64u * j) : 0u;
+        const u64 wm = (ones ? w[j] : ~w[j]) & (vb >= 64 ? ~0ull : (1ull << vb) - 1ull);
+        const u32 pcj = __popcll(wm);
+        if (k > 0 && k <= pcj) {
+          pos = ((w0 + j) << 6) + select_in_word64(wm, k);
           k = 0;
         } else if (k > 0) {
-          k -= cw[j];
+          k -= pcj;
         }
       }
       const u64 si = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
-      if (si < cap) out[si] = pos;
+      u64* out = ones ? P.ones : P.zeros;
+      if (si < (ones ? P.ones_cap : P.zeros_cap)) out[si] = pos;
     }
   }
 }
 
-__global__ void __launch_bounds__(D_NT) dir_kernel(const __grid_constant__ DirParams P) {
-  const int lane = threadIdx.x & 31;
+constexpr int D_NT = 128;
+__global__ void __launch_bounds__(D_NT, 6) dir_kernel(const __grid_constant__ DirParams P) {
+  __shared__ u32 wsum[D_NT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u64 nw = (P.m + 63) >> 6;
   const u64 nblk = (P.m + kL1Bits - 1) / kL1Bits;
-  const u32 l2w = (u32)((1ull << P.l2_log) >> 6) - 1u;  // L2 block = l2w + 1 words
-  const bool pow2 = P.rate_log >= 0;
-  for (u64 b = (u64)blockIdx.x * (D_NT / 32) + (threadIdx.x >> 5); b < nblk;
-       b += (u64)gridDim.x * (D_NT / 32)) {
-    const u64 l1v = __ldg(P.l1 + b);
-    const u64 bw = b * (kL1Bits / 64);  // the block's first word
-    const u32 nbw = (u32)min((u64)(kL1Bits / 64), nw - bw);
-    u32 carry = 0;  // ones of the block before this step
-    for (u32 s = 0; s < nbw; s += 128) {
-      const u32 lw = s + 4 * (u32)lane;  // the lane's first word in the block
-      u64 w[4] = {0ull, 0ull, 0ull, 0ull};
-      if (lw + 4 <= nbw) {
-        const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(P.words + bw + lw));
-        const ulonglong2 c2 = __ldg(reinterpret_cast<const ulonglong2*>(P.words + bw + lw) + 1);
-        w[0] = a.x; w[1] = a.y; w[2] = c2.x; w[3] = c2.y;
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (lw + j < nbw) w[j] = __ldg(P.words + bw + lw + j);
-      }
-      u32 pc[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) pc[j] = __popcll(w[j]);
-      const u32 c = pc[0] + pc[1] + pc[2] + pc[3];
-      u32 inc = c;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const u32 y = __shfl_up_sync(FULLM, inc, d);
-        if (lane >= d) inc += y;
-      }
-      const u32 ex = carry + inc - c;  // ones of the block before word lw
-      carry += __shfl_sync(FULLM, inc, 31);
-      if (lw >= nbw) continue;
-      u32 pre = ex;
+  const u32 l2m = (u32)((1ull << P.l2_log) >> 6) - 1u;  // L2 block = l2m + 1 words
+  for (u64 b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const u64 w0 = b * (kL1Bits / 64) + 8 * (u64)tid;  // this thread's first word
+    u32 pc[8], c = 0;
+    if (w0 + 8 <= nw) {
+      const ulonglong2* src = reinterpret_cast<const ulonglong2*>(P.words + w0);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        if (lw + j < nbw && ((lw + j) & l2w) == 0)
-          P.l2[((bw + lw + j) << 6) >> P.l2_log] = (u16)pre;
+        const ulonglong2 v = __ldg(src + j);
+        pc[2 * j] = __popcll(v.x);
+        pc[2 * j + 1] = __popcll(v.y);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) pc[j] = w0 + j < nw ? __popcll(__ldg(P.words + w0 + j)) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c += pc[j];
+    u32 inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 y = __shfl_up_sync(FULLM, inc, d);
+      if (lane >= d) inc += y;
+    }
+    __syncthreads();  // wsum reuse across blocks
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    u32 wpre = 0;
+#pragma unroll
+    for (int k = 0; k < D_NT / 32; ++k) wpre += k < warp ? wsum[k] : 0u;
+    const u32 ex = wpre + inc - c;  // ones of the block before word w0
+    if (w0 < nw) {
+      u32 pre = ex;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (w0 + j < nw && ((u32)(w0 + j) & l2m) == 0) P.l2[((w0 + j) << 6) >> P.l2_log] = (u16)pre;
         pre += pc[j];
       }
-      // samples: only when a multiple of the rate falls in the lane's range
-      const u64 g0 = (bw + lw) << 6;  // the lane's first bit
-      const u32 valid = (u32)min((u64)256, P.m - g0);
-      const u64 ob = l1v + ex, zb = g0 - ob;
+      // select samples: ordinals (ob, ob + c] of ones, (zb, zb + zc] of zeros
+      const u64 l1v = __ldg(P.l1 + b);
+      const u64 ob = l1v + ex, g0 = w0 << 6, zb = g0 - ob;
+      const u32 valid = (u32)min((u64)512, P.m - g0);
       const u32 zc = valid - c;
-      const bool hit = pow2 ? (((ob + c) >> P.rate_log) != (ob >> P.rate_log)) ||
-                                  (((zb + zc) >> P.rate_log) != (zb >> P.rate_log))
-                            : ((ob + c) / P.rate != ob / P.rate) || ((zb + zc) / P.rate != zb / P.rate);
-      if (hit) dir_samples(P, ob, zb, bw + lw, w, valid);
+      const bool hit = P.rate_log >= 0
+                           ? (((ob + c) >> P.rate_log) != (ob >> P.rate_log)) ||
+                                 (((zb + zc) >> P.rate_log) != (zb >> P.rate_log))
+                           : ((ob + c) / P.rate != ob / P.rate) || ((zb + zc) / P.rate != zb / P.rate);
+      if (hit) dir_hit(P, w0, nw, valid, ob, zb, c, zc);
     }
   }
 }
@@ -2020,8 +2051,8 @@ cudaError_t launch_wcount0(const void* text, u64 n, int in_bytes, u32 thr, u32* 
 cudaError_t launch_dir(const DirParams& p, int sms, cudaStream_t st) {
   if (p.m == 0) return cudaSuccess;
   const u64 nblk = (p.m + kL1Bits - 1) / kL1Bits;
-  u64 blocks = (nblk + (D_NT / 32) - 1) / (D_NT / 32);
-  if (blocks > (u64)sms * 8) blocks = (u64)sms * 8;
+  u64 blocks = nblk;
+  if (blocks > (u64)sms * 16) blocks = (u64)sms * 16;
   dir_kernel<<<(unsigned)blocks, D_NT, 0, st>>>(p);
   return cudaGetLastError();
 }

@@ -1,6 +1,7 @@
-# A/B build timings: default library vs build/var_* variants, WT_DIR on/off
 set -x
 mkdir -p gpurun_out
+rm -f gpurun_out/ab.txt
+timeout 900 python -m pytest tests/test_large_gpu.py tests/test_parity_gpu.py -x -q > gpurun_out/pytest_large.txt 2>&1; tail -3 gpurun_out/pytest_large.txt
 run() {  # label, env...
   local label=$1; shift
   echo "== $label" >> gpurun_out/ab.txt
@@ -8,10 +9,12 @@ run() {  # label, env...
     env "$@" timeout 300 python tools/bench_build.py $a 2>&1 | tail -1 >> gpurun_out/ab.txt
   done
 }
-run base WT_X=1
-run scan2 WT_B200_LIB=build/var_scan2/libwt_b200.so
-run base_nodir WT_DIR=0
-run base_again WT_X=1
-run pairstage WT_PAIR_KERNEL=stage
+run sag_dir WT_X=1
+run nosag_dir WT_B200_LIB=build/var_nosag/libwt_b200.so
+run nosag_nodir WT_DIR=0 WT_B200_LIB=build/var_nosag/libwt_b200.so
+run sag_nodir WT_DIR=0
+run sag_dir_again WT_X=1
 cat gpurun_out/ab.txt
-timeout 900 python -m pytest tests/test_large_gpu.py -k "pair or block" -x -q > gpurun_out/pytest_pair.txt 2>&1; tail -3 gpurun_out/pytest_pair.txt
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launch_dir.csv python tools/bench_build.py --n-log 30 --sigma 256 --reps 0 > /dev/null 2>&1
+python tools/profile_summary.py launches gpurun_out/launch_dir.csv > gpurun_out/launch_dir.txt 2>&1; head -12 gpurun_out/launch_dir.txt
+timeout 900 python -m pytest tests/test_configs_gpu.py -x -q > gpurun_out/pytest_cfg.txt 2>&1; tail -3 gpurun_out/pytest_cfg.txt

@@ -1843,40 +1843,6 @@ __global__ void __launch_bounds__(1024) l1_scan_kernel(const u32* __restrict__ c
 // of the threads' popcounts gives every L2 prefix; a thread selects only when
 // an ordinal multiple of the rate falls in its 512 bits (~1 in 8 threads at
 // rate 4096).  Full occupancy keeps enough loads in flight.
-// the select samples of one dir_kernel thread's 512 bits (rare: reloads its
-// words from L1 / L2, so the hot path keeps nothing live for it)
-__device__ __noinline__ void dir_hit(const DirParams& P, u64 w0, u64 nw, u32 valid, u64 ob, u64 zb,
-                                     u32 c, u32 zc) {
-  u64 w[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) w[j] = w0 + j < nw ? __ldg(P.words + w0 + j) : 0ull;
-#pragma unroll
-  for (int kind = 0; kind < 2; ++kind) {
-    const bool ones = kind == 0;
-    const u64 base = ones ? ob : zb;
-    const u32 cnt = ones ? c : zc;
-    for (u64 qo = wnext_multiple(base, P.rate, P.rate_log); qo <= base + cnt; qo += P.rate) {
-      u32 k = (u32)(qo - base);
-      u64 pos = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const u32 vb = valid > 64u * j ? min(64u, valid - 64u * j) : 0u;
-        const u64 wm = (ones ? w[j] : ~w[j]) & (vb >= 64 ? ~0ull : (1ull << vb) - 1ull);
-        const u32 pcj = __popcll(wm);
-        if (k > 0 && k <= pcj) {
-          pos = ((w0 + j) << 6) + select_in_word64(wm, k);
-          k = 0;
-        } else if (k > 0) {
-          k -= pcj;
-        }
-      }
-      const u64 si = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
-      u64* out = ones ? P.ones : P.zeros;
-      if (si < (ones ? P.ones_cap : P.zeros_cap)) out[si] = pos;
-    }
-  }
-}
-
 constexpr int D_NT = 128;
 __global__ void __launch_bounds__(D_NT, 6) dir_kernel(const __grid_constant__ DirParams P) {
   __shared__ u32 wsum[D_NT / 32];
@@ -1921,16 +1887,44 @@ __global__ void __launch_bounds__(D_NT, 6) dir_kernel(const __grid_constant__ Di
         if (w0 + j < nw && ((u32)(w0 + j) & l2m) == 0) P.l2[((w0 + j) << 6) >> P.l2_log] = (u16)pre;
         pre += pc[j];
       }
-      // select samples: ordinals (ob, ob + c] of ones, (zb, zb + zc] of zeros
-      const u64 l1v = __ldg(P.l1 + b);
-      const u64 ob = l1v + ex, g0 = w0 << 6, zb = g0 - ob;
-      const u32 valid = (u32)min((u64)512, P.m - g0);
-      const u32 zc = valid - c;
-      const bool hit = P.rate_log >= 0
-                           ? (((ob + c) >> P.rate_log) != (ob >> P.rate_log)) ||
-                                 (((zb + zc) >> P.rate_log) != (zb >> P.rate_log))
-                           : ((ob + c) / P.rate != ob / P.rate) || ((zb + zc) / P.rate != zb / P.rate);
-      if (hit) dir_hit(P, w0, nw, valid, ob, zb, c, zc);
+    }
+    // select samples: ~two of each kind per warp step at rate 4096 -- a
+    // warp-uniform loop over the sample ordinals in the warp's range; the
+    // owning lane finds the word from its popcounts, loads it (L1) and selects
+    const u64 l1v = __ldg(P.l1 + b);
+    const u64 g0 = min(w0 << 6, P.m);
+    const u32 valid = (u32)min((u64)512, P.m - g0);
+    const u64 ob = l1v + ex, zb = g0 - ob;
+    const u32 zc = valid - c;
+#pragma unroll
+    for (int kind = 0; kind < 2; ++kind) {
+      const bool ones = kind == 0;
+      const u64 bl = ones ? ob : zb;
+      const u32 cl = ones ? c : zc;
+      const u64 bw = __shfl_sync(FULLM, bl, 0);
+      const u64 ew = __shfl_sync(FULLM, bl + cl, 31);
+      for (u64 qo = wnext_multiple(bw, P.rate, P.rate_log); qo <= ew; qo += P.rate) {
+        if (bl < qo && qo <= bl + cl) {
+          u32 k = (u32)(qo - bl), j = 0, vb = 64;
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {  // the word holding ordinal k
+            const u32 vbx = valid > 64u * x ? min(64u, valid - 64u * x) : 0u;
+            const u32 cx = ones ? pc[x] : vbx - pc[x];
+            if ((u32)x == j && k > cx) {
+              k -= cx;
+              j = x + 1;
+            } else if ((u32)x == j) {
+              vb = vbx;
+            }
+          }
+          const u64 wv = __ldg(P.words + w0 + j);
+          const u64 wm = (ones ? wv : ~wv) & (vb >= 64 ? ~0ull : (1ull << vb) - 1ull);
+          const u64 pos = ((w0 + j) << 6) + select_in_word64(wm, k);
+          const u64 si = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
+          u64* out = ones ? P.ones : P.zeros;
+          if (si < (ones ? P.ones_cap : P.zeros_cap)) out[si] = pos;
+        }
+      }
     }
   }
 }

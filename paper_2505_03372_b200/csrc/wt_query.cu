@@ -181,180 +181,6 @@ __global__ void __launch_bounds__(Q_NT) select_kernel(const __grid_constant__ Tr
     st_stream_i64(out + i, (i64)p, pol);
 }
 
-// ---------------------------------------------------------------------------
-// Unsorted batches: two queries per thread (q and q + Q_NT of the CTA's
-// 2 Q_NT), their level walks interleaved -- each level's two line loads are
-// in flight together (one query per thread leaves the walks latency bound:
-// ~95 % long-scoreboard stalls at full occupancy).  Same contract as the
-// one-query kernels above (validation, first bad index, output forms).
-// ---------------------------------------------------------------------------
-constexpr int QPT = 2;
-template <int kOut, bool kValidate>
-__global__ void __launch_bounds__(Q_NT) access2_kernel(const __grid_constant__ TreeDev T,
-                                                       const i64* __restrict__ pos,
-                                                       void* __restrict__ out, u64 m, u64 base,
-                                                       u64* __restrict__ bad) {
-  const u64 q0 = (u64)blockIdx.x * (Q_NT * QPT) + threadIdx.x;
-  const u64 pol = l2_evict_first_policy();
-  u64 p[QPT];
-  u32 key[QPT];
-  int id[QPT];
-  bool live[QPT];
-#pragma unroll
-  for (int j = 0; j < QPT; ++j) {
-    const u64 q = q0 + (u64)j * Q_NT;
-    live[j] = q < m;
-    p[j] = live[j] ? (u64)ld_stream_i64(pos + q, pol) : 0ull;
-    if (kValidate && live[j] && p[j] >= T.n) {
-      atomicMin(bad, base + q);
-      live[j] = false;
-    }
-    key[j] = 0;
-    id[j] = -1;
-  }
-  for (u32 l = 0; l < T.L; ++l) {
-    u32 bit[QPT];
-    u64 r1[QPT];
-#pragma unroll
-    for (int j = 0; j < QPT; ++j)
-      if (live[j] && id[j] < 0) r1[j] = qrank1_bit(T.ql[l], p[j], bit[j]);
-#pragma unroll
-    for (int j = 0; j < QPT; ++j) {
-      if (!live[j] || id[j] >= 0) continue;
-      const NodeEnt* ne = T.lv[l].nodes + key[j];
-      const int leaf = __ldg(&ne->leaf[bit[j]]);
-      if (leaf >= 0) {
-        id[j] = leaf;
-        continue;
-      }
-      p[j] = bit[j] ? r1[j] + (u64)__ldg(&ne->one_base) : (p[j] - r1[j]) + (u64)__ldg(&ne->zero_base);
-      key[j] = (key[j] << 1) | bit[j];
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < QPT; ++j) {
-    if (!live[j]) continue;
-    const u64 i = q0 + (u64)j * Q_NT;
-    const int d = id[j] < 0 ? 0 : id[j];
-    if (kOut == 8) {
-      reinterpret_cast<i64*>(out)[i] = d;
-    } else {
-      const u16 sym = __ldg(T.symbols + d);
-      if (kOut == 1)
-        reinterpret_cast<u8*>(out)[i] = (u8)sym;
-      else
-        reinterpret_cast<u16*>(out)[i] = sym;
-    }
-  }
-}
-
-template <bool kValidate>
-__global__ void __launch_bounds__(Q_NT) rank2_kernel(const __grid_constant__ TreeDev T,
-                                                     const i64* __restrict__ ids,
-                                                     const i64* __restrict__ pos,
-                                                     i64* __restrict__ out, u64 m, u64 base,
-                                                     u64* __restrict__ bad) {
-  const u64 q0 = (u64)blockIdx.x * (Q_NT * QPT) + threadIdx.x;
-  const u64 pol = l2_evict_first_policy();
-  u64 p[QPT];
-  u32 c[QPT], code[QPT], len[QPT];
-  bool live[QPT];
-  u32 lmax = 0;
-#pragma unroll
-  for (int j = 0; j < QPT; ++j) {
-    const u64 q = q0 + (u64)j * Q_NT;
-    live[j] = q < m;
-    c[j] = 0;
-    p[j] = 0;
-    if (live[j]) {
-      p[j] = (u64)pos[q];
-      if (!symbol_id<kValidate>(T, ids[q], c[j]) || (kValidate && p[j] > T.n)) {
-        atomicMin(bad, base + q);
-        live[j] = false;
-      }
-    }
-    const u32 cd = live[j] ? __ldg(T.id_code + c[j]) : 0u;
-    code[j] = cd & 0xffffu;
-    len[j] = cd >> 16;
-    lmax = max(lmax, len[j]);
-  }
-  for (u32 l = 0; l < lmax; ++l) {
-    u64 r1[QPT];
-#pragma unroll
-    for (int j = 0; j < QPT; ++j)
-      if (l < len[j]) r1[j] = qrank1(T.ql[l], p[j]);
-#pragma unroll
-    for (int j = 0; j < QPT; ++j) {
-      if (l >= len[j]) continue;
-      const u32 bit = (code[j] >> (T.L - 1 - l)) & 1u;
-      const u32 key = code[j] >> (T.L - l);
-      const NodeEnt* ne = T.lv[l].nodes + key;
-      const u64 nb = bit ? (u64)__ldg(&ne->one_base) : (u64)__ldg(&ne->zero_base);
-      p[j] = (bit ? r1[j] : p[j] - r1[j]) + nb;
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < QPT; ++j)
-    if (live[j]) st_stream_i64(out + q0 + (u64)j * Q_NT, (i64)(p[j] - (u64)__ldg(T.cum + c[j])), pol);
-}
-
-template <bool kValidate>
-__global__ void __launch_bounds__(Q_NT) select2_kernel(const __grid_constant__ TreeDev T,
-                                                       const i64* __restrict__ ids,
-                                                       const i64* __restrict__ ks,
-                                                       i64* __restrict__ out, u64 m, u64 base,
-                                                       u64* __restrict__ bad) {
-  const u64 q0 = (u64)blockIdx.x * (Q_NT * QPT) + threadIdx.x;
-  const u64 pol = l2_evict_first_policy();
-  u64 p[QPT];
-  u32 code[QPT];
-  int len[QPT];
-  bool live[QPT];
-  int lmax = 0;
-#pragma unroll
-  for (int j = 0; j < QPT; ++j) {
-    const u64 q = q0 + (u64)j * Q_NT;
-    live[j] = q < m;
-    u32 c = 0;
-    i64 k = 1;
-    if (live[j]) {
-      k = ks[q];
-      if (!symbol_id<kValidate>(T, ids[q], c) ||
-          (kValidate && (k < 1 || k > __ldg(T.cum + c + 1) - __ldg(T.cum + c)))) {
-        atomicMin(bad, base + q);
-        live[j] = false;
-      }
-    }
-    const u32 cd = live[j] ? __ldg(T.id_code + c) : 0u;
-    code[j] = cd & 0xffffu;
-    len[j] = (int)(cd >> 16);
-    p[j] = live[j] ? (u64)__ldg(T.cum + c) + (u64)k - 1 : 0ull;
-    lmax = max(lmax, len[j]);
-  }
-  // bottom-up: query j walks levels len[j]-1 .. 0; step s = lmax-1 .. 0 takes
-  // level s of every query with s < len
-  for (int l = lmax - 1; l >= 0; --l) {
-    u64 arg[QPT];
-    bool one[QPT];
-#pragma unroll
-    for (int j = 0; j < QPT; ++j) {
-      if (l >= len[j]) continue;
-      one[j] = (code[j] >> (T.L - 1 - l)) & 1u;
-      const u32 key = code[j] >> (T.L - l);
-      const NodeEnt* ne = T.lv[l].nodes + key;
-      arg[j] = p[j] - (one[j] ? (u64)__ldg(&ne->one_base) : (u64)__ldg(&ne->zero_base)) + 1;
-    }
-#pragma unroll
-    for (int j = 0; j < QPT; ++j) {
-      if (l >= len[j]) continue;
-      p[j] = one[j] ? qselect<true>(T.ql[l], arg[j]) : qselect<false>(T.ql[l], arg[j]);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < QPT; ++j)
-    if (live[j]) st_stream_i64(out + q0 + (u64)j * Q_NT, (i64)p[j], pol);
-}
-
 template <bool V>
 static void launch_q(const TreeDev& T, int kind, int out_kind, const i64* ids, const i64* args,
                      void* out, u64 m, int rate_log, u64 base, u64* bad, bool packed,
@@ -384,26 +210,6 @@ cudaError_t launch_query(const TreeDev& T, int kind, int out_kind, bool validate
   if (kind < 0 || kind > 2) return cudaErrorInvalidValue;
   const u64 blocks = (m + Q_NT - 1) / Q_NT;
   if (blocks > 0x7fffffffull) return cudaErrorInvalidValue;
-  static const bool two = !(getenv("WT_QPT") && getenv("WT_QPT")[0] == '1');  // A/B knob
-  if (!packed && two) {  // unsorted batches: two interleaved walks per thread
-    const unsigned b2 = (unsigned)((m + 2 * Q_NT - 1) / (2 * Q_NT));
-    if (kind == 0) {
-#define WT_A2(K, V) access2_kernel<K, V><<<b2, Q_NT, 0, st>>>(T, args, out, m, base, bad)
-      if (validate) {
-        if (out_kind == 8) WT_A2(8, true); else if (out_kind == 1) WT_A2(1, true); else WT_A2(2, true);
-      } else {
-        if (out_kind == 8) WT_A2(8, false); else if (out_kind == 1) WT_A2(1, false); else WT_A2(2, false);
-      }
-#undef WT_A2
-    } else if (kind == 1) {
-      if (validate) rank2_kernel<true><<<b2, Q_NT, 0, st>>>(T, ids, args, (i64*)out, m, base, bad);
-      else rank2_kernel<false><<<b2, Q_NT, 0, st>>>(T, ids, args, (i64*)out, m, base, bad);
-    } else {
-      if (validate) select2_kernel<true><<<b2, Q_NT, 0, st>>>(T, ids, args, (i64*)out, m, base, bad);
-      else select2_kernel<false><<<b2, Q_NT, 0, st>>>(T, ids, args, (i64*)out, m, base, bad);
-    }
-    return cudaGetLastError();
-  }
   if (validate)
     launch_q<true>(T, kind, out_kind, ids, args, out, m, rate_log, base, bad, packed, (unsigned)blocks, st);
   else

@@ -1905,18 +1905,27 @@ __global__ void __launch_bounds__(D_NT, 6) dir_kernel(const __grid_constant__ Di
       const u64 ew = __shfl_sync(FULLM, bl + cl, 31);
       for (u64 qo = wnext_multiple(bw, P.rate, P.rate_log); qo <= ew; qo += P.rate) {
         if (bl < qo && qo <= bl + cl) {
-          u32 k = (u32)(qo - bl), j = 0, vb = 64;
+          // the word holding ordinal k: binary search over the word counts
+          // (zeros: the valid bits of the word minus its ones)
+          u32 k = (u32)(qo - bl);
+          u32 cw[8];
 #pragma unroll
-          for (int x = 0; x < 8; ++x) {  // the word holding ordinal k
+          for (int x = 0; x < 8; ++x) {
             const u32 vbx = valid > 64u * x ? min(64u, valid - 64u * x) : 0u;
-            const u32 cx = ones ? pc[x] : vbx - pc[x];
-            if ((u32)x == j && k > cx) {
-              k -= cx;
-              j = x + 1;
-            } else if ((u32)x == j) {
-              vb = vbx;
-            }
+            cw[x] = ones ? pc[x] : vbx - pc[x];
           }
+          const u32 q0c = cw[0] + cw[1] + cw[2] + cw[3];
+          const bool hi4 = k > q0c;
+          k -= hi4 ? q0c : 0u;
+          const u32 a0 = hi4 ? cw[4] : cw[0], a1 = hi4 ? cw[5] : cw[1];
+          const u32 a2 = hi4 ? cw[6] : cw[2], a3 = hi4 ? cw[7] : cw[3];
+          const bool hi2 = k > a0 + a1;
+          k -= hi2 ? a0 + a1 : 0u;
+          const u32 b0 = hi2 ? a2 : a0;
+          const bool hi1 = k > b0;
+          k -= hi1 ? b0 : 0u;
+          const u32 j = (hi4 ? 4u : 0u) + (hi2 ? 2u : 0u) + (hi1 ? 1u : 0u);
+          const u32 vb = valid > 64u * j ? min(64u, valid - 64u * j) : 0u;
           const u64 wv = __ldg(P.words + w0 + j);
           const u64 wm = (ones ? wv : ~wv) & (vb >= 64 ? ~0ull : (1ull << vb) - 1ull);
           const u64 pos = ((w0 + j) << 6) + select_in_word64(wm, k);

@@ -2,7 +2,8 @@
 realistic size, for one `ncu --set full` capture of all of them
 (scripts/gpu_ncu_all.sh; summary: profiles/rNN_ncu_all_kernels.txt).
 
-  C2 build (u8, sigma=256, block mode)   hist8_blocks, block_l1, l1_scan, wlevel<u8,u8>, wlast, qlayout
+  C2 build (u8, sigma=256, block mode)   hist8_blocks, block_l1, l1_scan, wlevel<u8,u8,1>, wpair, dir, qlayout
+  2^24 u8 builds                          wlevel tile mode, wcount0, dirq (WT_DIRQ=1)
   u8 LUT build (sigma=200, 2^28)          hist8, wcount0, wlevel<u8,u8,lut>, wlast<lut>
   C3u-like build (u16, 2^28)              hist16p, hist16_fold, wlevel<u16,u16>
   declared alphabet with a stray symbol   first_outside
@@ -29,6 +30,14 @@ rng = np.random.default_rng(3)
 n = 1 << 30
 text = torch.randint(0, 256, (n,), generator=g, device=dev, dtype=torch.int32).to(torch.uint8)
 t = W.construct(text)
+del text
+# tile mode (2^24 symbols: too few L1 blocks for block mode) and the opt-in
+# one-pass directory + query layout (dirq_kernel)
+text = torch.randint(0, 256, (1 << 24,), generator=g, device=dev, dtype=torch.int32).to(torch.uint8)
+del W.construct(text).handle
+os.environ["WT_DIRQ"] = "1"
+del W.construct(text).handle
+os.environ.pop("WT_DIRQ")
 del text
 # u8 LUT levels + per-tile counting (not block mode: 2^28 symbols, sigma=200)
 text = torch.randint(0, 200, (1 << 28,), generator=g, device=dev, dtype=torch.int32).to(torch.uint8)

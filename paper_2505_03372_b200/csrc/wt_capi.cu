@@ -800,6 +800,27 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
         // launch (a streaming pass over its bits) instead of inside the level
         // kernel (WT_DIR=0: inside)
         wp.skip_dir = dir_after && wp.out ? 1 : 0;
+        wp.plut_shift = 0xffu;
+        if (l == 0 && dlut && sym_bytes == 1 && P.sigma <= 8) {
+          // a shift making (symbol >> s) & 7 distinct over the alphabet: the
+          // codes then come from an 8-byte register table (pair kernel)
+          for (uint32_t sh = 0; sh <= 5 && wp.plut_shift == 0xffu; ++sh) {
+            uint32_t seen = 0, lo = 0, hi = 0;
+            bool ok = true;
+            for (uint32_t i = 0; i < P.sigma && ok; ++i) {
+              const uint32_t ix = (P.symbols[i] >> sh) & 7u;
+              ok = !((seen >> ix) & 1u);
+              seen |= 1u << ix;
+              const uint32_t code = P.values[i] & 0xffu;
+              if (ix < 4) lo |= code << (8 * ix); else hi |= code << (8 * (ix - 4));
+            }
+            if (ok) {
+              wp.plut_shift = sh;
+              wp.plut_lo = lo;
+              wp.plut_hi = hi;
+            }
+          }
+        }
         CU(launch_wlevel(wp, in_bytes, P.code_bytes, l == 0 && dlut != nullptr, sm_count(device), st));
         if (wp.skip_dir || (dirq_on && wp.m)) TRY(level_dir(l, wp.words));
         ci ^= 1;

@@ -30,6 +30,9 @@ struct WLevelParams {
   // two bits at a LUT level 0 (bit l+1 = parity of symbol >= nthr[i])
   int next_block;
   int skip_dir;            // L2 entries / samples left to dir_kernel (fast tiles)
+  // small alphabets at a u8 LUT level: code = byte plut_lo|hi[(sym >> plut_shift)
+  // & 7] -- one PRMT per 4 symbols instead of 4 table loads (0xff: unused)
+  u32 plut_shift, plut_lo, plut_hi;
   u32 nthr[3];
   u32 thr;                 // level 0 with a LUT: smallest symbol whose code has the top bit
   u32 shift_bit;           // L-1-l

@@ -1409,10 +1409,18 @@ __global__ void __launch_bounds__(256) wlast_kernel(const __grid_constant__ WLev
 // reads of a warp spread over all banks.
 // ---------------------------------------------------------------------------
 template <typename TIn, typename TC>
-__device__ __forceinline__ void wp_codes(uint4& q, const u16* slut, const u16* glut, bool lut) {
+__device__ __forceinline__ void wp_codes(uint4& q, const u16* slut, const u16* glut, bool lut,
+                                         const WLevelParams& P) {
   // 16 input bytes -> 16 code bytes (u8 codes) or 8 code halfwords (u16)
   if (!lut) return;
-  if (sizeof(TIn) == 1) {  // u8 text, u8 codes (L = 2 here)
+  if (sizeof(TIn) == 1 && P.plut_shift != 0xffu) {  // <= 8 symbols: a register table
+    auto map4 = [&](u32 x) -> u32 {
+      const u32 y = (x >> P.plut_shift) & 0x07070707u;  // 3-bit index per byte
+      const u32 t = y | (y >> 4);                       // nibbles 0, 1 in byte 0; 2, 3 in byte 2
+      return __byte_perm(P.plut_lo, P.plut_hi, __byte_perm(t, 0u, 0x4420u));
+    };
+    q = make_uint4(map4(q.x), map4(q.y), map4(q.z), map4(q.w));
+  } else if (sizeof(TIn) == 1) {  // u8 text, u8 codes (L = 2 here)
     auto map4 = [&](u32 x) -> u32 {
       return (u32)slut[x & 0xffu] | ((u32)slut[(x >> 8) & 0xffu] << 8) |
              ((u32)slut[(x >> 16) & 0xffu] << 16) | ((u32)slut[x >> 24] << 24);
@@ -1554,7 +1562,7 @@ __global__ void __launch_bounds__(256, 2) wpair_kernel(const __grid_constant__ W
     for (int k = 0; k < K; ++k) {
       const u32 c = (u32)k ^ ((u32)lane & 7u);
       q[k] = *reinterpret_cast<const uint4*>(src + c * 16);
-      wp_codes<TIn, TC>(q[k], slut, P.lut, kLut);
+      wp_codes<TIn, TC>(q[k], slut, P.lut, kLut, P);
       u32 mk = 0;
 #pragma unroll
       for (int s2 = 0; s2 < NS; ++s2) {

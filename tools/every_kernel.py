@@ -34,9 +34,11 @@ del text
 # tile mode (2^24 symbols: too few L1 blocks for block mode) and the opt-in
 # one-pass directory + query layout (dirq_kernel)
 text = torch.randint(0, 256, (1 << 24,), generator=g, device=dev, dtype=torch.int32).to(torch.uint8)
-del W.construct(text).handle
+t24 = W.construct(text)
+del t24
 os.environ["WT_DIRQ"] = "1"
-del W.construct(text).handle
+t24 = W.construct(text)
+del t24
 os.environ.pop("WT_DIRQ")
 del text
 # u8 LUT levels + per-tile counting (not block mode: 2^28 symbols, sigma=200)

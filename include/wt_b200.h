@@ -103,6 +103,10 @@ extern "C" {
 #define WT_A_ZEROS       10   /* i64[n_zeros] per level                      */
 #define WT_A_NODE_STARTS 11   /* i64[n_nodes] per level                      */
 #define WT_A_NODE_RANK0  12   /* i64[n_nodes] per level                      */
+/* query-side layout (this engine's own, not part of the index format):     */
+#define WT_A_QLINES      13   /* u64[4 * n_lines] per level: [ones before | 3 words] */
+#define WT_A_QSEL1       14   /* u32 per level: line of every 64-th one           */
+#define WT_A_QSEL0       15   /* u32 per level: line of every 64-th zero          */
 
 typedef struct wt_tree wt_tree;
 typedef struct wt_bits wt_bits;

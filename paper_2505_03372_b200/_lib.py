@@ -32,7 +32,7 @@ Q_ACCESS, Q_RANK, Q_SELECT = 0, 1, 2
 B_RANK1, B_RANK0, B_SELECT1, B_SELECT0, B_BIT = range(5)
 F_DEVICE_PTRS, F_SYMBOLS, F_ACCESS_IDS, F_SORT, F_PHASES = 1, 2, 4, 8, 16
 (A_SYMBOLS, A_CODE_VALUES, A_CODE_LENS, A_CUM_HIST, A_LEVEL_SIZES, A_REGION_OFFS, A_WORDS,
- A_L1, A_L2, A_ONES, A_ZEROS, A_NODE_STARTS, A_NODE_RANK0) = range(13)
+ A_L1, A_L2, A_ONES, A_ZEROS, A_NODE_STARTS, A_NODE_RANK0, A_QLINES, A_QSEL1, A_QSEL0) = range(16)
 
 
 class Meta(C.Structure):

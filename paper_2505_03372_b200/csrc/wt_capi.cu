@@ -710,13 +710,13 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       const bool pair_ok = !(pe && pe[0] == '0');
       const char* de = getenv("WT_DIR");
       const char* qe = getenv("WT_DIRQ");
-      // After each partitioning level's kernel, dir_kernel writes its L2
-      // entries + select samples (a streaming pass over its bits; WT_DIR=0:
-      // inside the level kernel); WT_DIRQ=1: dirq_kernel writes them together
-      // with the level's query lines (measured slower: latency bound)
-      const bool dirq_on = qe && qe[0] == '1';
+      // After each level's kernel, dirq_kernel writes its L2 entries + select
+      // samples together with its query lines (one streaming pass over the
+      // level's bits).  WT_DIRQ=0: dir_kernel for the directory (WT_DIR=0:
+      // inside the level kernel) and qlayout_kernel for the lines (A/B)
+      const bool dirq_on = !(qe && qe[0] == '0');
       const bool dir_after = dirq_on || !(de && de[0] == '0');
-      auto level_dir = [&](uint32_t lv, const u64* words) -> int {
+      auto level_dir = [&](uint32_t lv, const u64* words, bool pdl) -> int {
         LevelHost& hl = t->lv[lv];
         const uint64_t mm = hl.meta.n_bits;
         DirParams dp{};
@@ -744,8 +744,16 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
         q.sel0 = hl.sel0;
         q.cap1 = hl.sel_cap;
         q.cap0 = hl.sel_cap;
-        CU(launch_dirq(q, sm_count(device), st));
+        CU(launch_dirq(q, sm_count(device), st, pdl));
         q_done[lv] = 1;
+        return WT_OK;
+      };
+      // L1 directory of level lv from its per-L1-block counts (l1cnt[cidx])
+      std::vector<char> scanned(P.L + 1, 0);
+      auto scan_level = [&](uint32_t lv, int cidx) -> int {
+        LevelHost& hs = t->lv[lv];
+        CU(launch_l1_scan(l1cnt[cidx], hs.meta.n_l1, hs.l1, totals + lv, st));
+        scanned[lv] = 1;
         return WT_OK;
       };
       int ci = 0;
@@ -755,7 +763,7 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
         if (m == 0) continue;
         const int in_bytes = l == 0 ? sym_bytes : P.code_bytes;
         LevelHost& h = t->lv[l];
-        CU(launch_l1_scan(l1cnt[ci], h.meta.n_l1, h.l1, totals + l, st));
+        if (!scanned[l]) TRY(scan_level(l, ci));
         const bool pair = pair_ok && l + 2 == P.L && (uint64_t)P.sizes[l + 1] == m;
         const bool next_blk = !pair && l + 1 < P.L && blk[l] && blk[l + 1];
         WLevelParams wp{};
@@ -822,13 +830,20 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
           }
         }
         CU(launch_wlevel(wp, in_bytes, P.code_bytes, l == 0 && dlut != nullptr, sm_count(device), st));
-        if (wp.skip_dir || (dirq_on && wp.m)) TRY(level_dir(l, wp.words));
         ci ^= 1;
+        // The next level's L1 scan (its counts came from this level's kernel)
+        // goes ahead of this level's directory pass, which is launched as its
+        // programmatic dependent: the one-CTA scan overlaps the streaming pass.
+        bool pdl = false;
+        if (dirq_on && l + 1 < P.L && P.sizes[l + 1] && (wp.out || pair)) {
+          TRY(scan_level(l + 1, ci));
+          pdl = true;
+        }
+        if (wp.skip_dir || (dirq_on && wp.m)) TRY(level_dir(l, wp.words, pdl));
         if (pair) {  // the last level: L1 from the pair pass's counts, then L2 + samples
-          LevelHost& hn = t->lv[l + 1];
           CU(cudaEventRecord(lev[l + 1], st));
-          CU(launch_l1_scan(l1cnt[ci], hn.meta.n_l1, hn.l1, totals + l + 1, st));
-          TRY(level_dir(l + 1, wp.next_words));
+          if (!scanned[l + 1]) TRY(scan_level(l + 1, ci));
+          TRY(level_dir(l + 1, wp.next_words, false));
           break;
         }
       }
@@ -984,6 +999,17 @@ extern "C" int wt_tree_get(const wt_tree* t, int what, uint32_t level, void* dst
     case WT_A_ONES: return copy_out(dst, t->lv[level].ones, t->lv[level].meta.n_ones * 8, cap, true);
     case WT_A_ZEROS:
       return copy_out(dst, t->lv[level].zeros, t->lv[level].meta.n_zeros * 8, cap, true);
+    case WT_A_QLINES:
+      return copy_out(dst, t->lv[level].lines, t->lv[level].n_lines * kQLineBytes, cap, true);
+    case WT_A_QSEL1:
+    case WT_A_QSEL0: {
+      // the filled prefix: one entry per 2^kQSelLog ones / zeros
+      const wt_level_meta& m = t->lv[level].meta;
+      const u64 k = what == WT_A_QSEL1 ? m.total_ones : m.n_bits - m.total_ones;
+      const u64 cnt = std::min<u64>((k + (1u << kQSelLog) - 1) >> kQSelLog, t->lv[level].sel_cap);
+      return copy_out(dst, what == WT_A_QSEL1 ? t->lv[level].sel1 : t->lv[level].sel0, cnt * 4, cap,
+                      true);
+    }
     case WT_A_NODE_STARTS:
     case WT_A_NODE_RANK0: {
       std::lock_guard<std::mutex> lk(const_cast<wt_tree*>(t)->tables_mutex);

@@ -121,7 +121,10 @@ struct DirQParams {
   u32* sel0;
   u64 cap1, cap0;
 };
-cudaError_t launch_dirq(const DirQParams& p, int sms, cudaStream_t st);
+// pdl: launched as a programmatic dependent of the preceding kernel on `st`
+// (an l1_scan_kernel, which releases it at its start): the two overlap.  The
+// directory pass reads nothing that kernel writes.
+cudaError_t launch_dirq(const DirQParams& p, int sms, cudaStream_t st, bool pdl = false);
 cudaError_t launch_qlayout(const LevelDev& L, const u64* total, u32 l2_shift, ulonglong2* lines,
                            u64 n_lines, u32* sel1, u64 cap1, u32* sel0, u64 cap0, cudaStream_t st);
 

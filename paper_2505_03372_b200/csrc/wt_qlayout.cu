@@ -7,6 +7,7 @@
 // the select samples (line index of every 2^kQSelLog-th one / zero) that
 // fall in its line.  The last line is a sentinel whose header is the level
 // total.
+#include <atomic>
 #include "wt_common.cuh"
 #include "wt_kernels.h"
 #include "wt_rs.cuh"
@@ -71,143 +72,243 @@ u64 qlayout_lines(u64 n_bits) { return n_bits / kQBits + 1; }
 // ---------------------------------------------------------------------------
 // dirq_kernel: the reference directory (L2 entries, select samples every
 // `rate`-th one / zero, rankselect.py:495-532) and the query layout (lines +
-// line samples) of one level in ONE streaming pass over its bits.  A CTA of
-// 1024 threads owns 1024 consecutive lines = 3072 words = three whole L1
-// blocks, so it starts on both a line and an L1 boundary: thread t holds
-// line t (three words), a CTA scan of the line popcounts on top of l1[3 g]
-// gives every line header; the L2 entry of word w = (ones before w) -
-// l1[w >> 10].  Reference samples (~two of each kind per warp at rate 4096):
-// a warp-uniform loop over the ordinals in the warp's range, the owning lane
-// selects in its line.
+// line samples) of one level in ONE streaming pass over its bits (replaces
+// dir_kernel + qlayout_kernel on the build path).
+//
+// A 256-thread CTA owns 1024 consecutive lines = 3072 words = three whole L1
+// blocks, so it starts on both a line and an L1 boundary and needs no look-up
+// into a directory.  Thread t owns lines [4t, 4t + 4) = words [12t, 12t + 12)
+// (six 16-byte loads, all in flight at once); one warp scan of the thread
+// counts and one barrier for the warp sums give every line header on top of
+// l1[3 g].  Each line leaves as one 32-byte store (a whole sector).  Inside
+// the CTA everything is 32-bit: the L2 entry of word w is (ones of the CTA
+// before w) - (l1[w >> 10] - l1[3 g]); a line holds at most three line
+// samples of each kind.  Reference samples (~three of each kind per warp at
+// rate 4096): a warp-uniform loop over the ordinals of the warp's range, the
+// owning lane selects in its twelve words.
 // ---------------------------------------------------------------------------
-constexpr int DQ_NT = 1024;  // threads = lines per CTA (3 L1 blocks: kQW = 3)
-static_assert(kQW == 3, "dirq_kernel aligns three L1 blocks with 1024 lines of 3 words");
+constexpr int DQ_NT = 256;                 // threads per CTA
+constexpr int DQ_LPT = 4;                  // lines per thread
+constexpr int DQ_WPT = DQ_LPT * 3;         // words per thread
+constexpr int DQ_LINES = DQ_LPT * DQ_NT;   // lines per CTA
+static_assert(kQW == 3 && DQ_LINES * kQW == 3 * (kL1Bits / 64),
+              "dirq_kernel aligns three L1 blocks with 1024 lines of 3 words");
+static_assert((1 << kQSelLog) >= kQBits / 3, "at most three line samples per line");
 
 __device__ __forceinline__ u64 dq_next_multiple(u64 o, u64 rate, int rate_log) {
   if (rate_log >= 0) return ((o >> rate_log) + 1) << rate_log;
   return (o / rate + 1) * rate;
 }
 
-__global__ void __launch_bounds__(DQ_NT) dirq_kernel(const __grid_constant__ DirQParams Q) {
+__device__ __forceinline__ void dq_store_line(ulonglong2* p, u64 a, u64 b, u64 c, u64 d) {
+  asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d)
+               : "memory");
+}
+
+// line samples of one kind: sel[j] = line for every j with j * 2^kQSelLog + 1
+// in (before, before + cnt] (at most three: cnt <= 192)
+__device__ __forceinline__ void dq_line_samples(u32* sel, u64 cap, u64 before, u32 cnt, u32 line) {
+  const u64 j0 = (before + (1u << kQSelLog) - 1) >> kQSelLog;
+  const u32 k = (u32)(((before + cnt + (1u << kQSelLog) - 1) >> kQSelLog) - j0);
+#pragma unroll
+  for (u32 x = 0; x < 3; ++x)
+    if (x < k && j0 + x < cap) sel[j0 + x] = line;
+}
+
+__device__ __forceinline__ u32 dq_smem(const void* p) {
+  return (u32)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void dq_load_group(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(dq_smem(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dq_smem(dst)),
+      "l"(src), "r"(bytes), "r"(dq_smem(bar))
+      : "memory");
+}
+__device__ __forceinline__ void dq_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(dq_smem(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int DQ_GWORDS = 3 * (kL1Bits / 64);  // words per CTA group (3072)
+constexpr int DQ_GBYTES = DQ_GWORDS * 8;       // 24 KiB
+constexpr int DQ_SMEM = 2 * DQ_GBYTES + 64;    // two group buffers + mbarriers
+
+// Persistent: CTA b takes groups b, b + grid, ...; the next group's 24 KiB
+// stream into the other shared buffer by one bulk copy (cp.async.bulk +
+// mbarrier) while this one is processed, so each SM keeps ~100 KiB of reads in
+// flight without spending registers on them.  The level's partial last
+// group (its words end inside it) loads directly from global memory.
+__global__ void __launch_bounds__(DQ_NT, 3) dirq_kernel(const __grid_constant__ DirQParams Q) {
   const DirParams& P = Q.d;
-  __shared__ u32 wsum[32];
+  extern __shared__ __align__(128) u8 dq_sm[];
+  u64* buf = reinterpret_cast<u64*>(dq_sm);
+  u64* mbar = reinterpret_cast<u64*>(dq_sm + 2 * DQ_GBYTES);
+  __shared__ u32 wsum[2][DQ_NT / 32];
   const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u64 nw = (P.m + 63) >> 6;
   const u64 n_l1 = (P.m + kL1Bits - 1) / kL1Bits;
-  const u64 ncta = (Q.n_lines + DQ_NT - 1) / DQ_NT;
-  const u32 l2m = (u32)((1ull << P.l2_log) >> 6) - 1u;  // L2 block = l2m + 1 words
+  const u32 l2m = (u32)((1ull << P.l2_log) >> 6) - 1u;  // L2 block = l2m + 1 words (<= 1024)
+  const u32 l2wl = P.l2_log - 6;
+  const u64 ng = (Q.n_lines + DQ_LINES - 1) / DQ_LINES;
+  const u64 gfull = nw / DQ_GWORDS;  // groups whose words all lie inside the level
   const u64 total = *Q.total;
-  // the next group's words are loaded while this group is processed
-  u64 wn[3];
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(dq_smem(&mbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(dq_smem(&mbar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (u32 k = 0; k < 2; ++k) {
+      const u64 gg = blockIdx.x + (u64)k * gridDim.x;
+      if (gg < gfull) dq_load_group(buf + k * DQ_GWORDS, P.words + gg * DQ_GWORDS, DQ_GBYTES, &mbar[k]);
+    }
+  }
+  __syncthreads();
+  u32 it = 0;
+  for (u64 g = blockIdx.x; g < ng; g += gridDim.x, ++it) {
+  const u32 slot = it & 1u;
+  const u64 gw0 = g * DQ_GWORDS;                 // the CTA's first word
+  const u64 w0 = gw0 + (u64)tid * DQ_WPT;        // this thread's first word
+  u64 w[DQ_WPT];
+  if (g < gfull) {
+    dq_wait(&mbar[slot], (it >> 1) & 1u);
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(buf + slot * DQ_GWORDS + tid * DQ_WPT);
+#pragma unroll
+    for (int j = 0; j < DQ_WPT / 2; ++j) {
+      const ulonglong2 v = src[j];
+      w[2 * j] = v.x;
+      w[2 * j + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < DQ_WPT; ++j) w[j] = w0 + j < nw ? __ldg(P.words + w0 + j) : 0ull;  // padding bits are zero
+  }
+  const u64 l1a = 3 * g < n_l1 ? __ldg(P.l1 + 3 * g) : total;  // ones before the CTA
+  const u32 d1 = 3 * g + 1 < n_l1 ? (u32)(__ldg(P.l1 + 3 * g + 1) - l1a) : 0u;
+  const u32 d2 = 3 * g + 2 < n_l1 ? (u32)(__ldg(P.l1 + 3 * g + 2) - l1a) : 0u;
+  u32 pc[DQ_WPT], c = 0;
+#pragma unroll
+  for (int j = 0; j < DQ_WPT; ++j) {
+    pc[j] = __popcll(w[j]);
+    c += pc[j];
+  }
+  u32 inc = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= (u32)d) inc += y;
+  }
+  if (lane == 31) wsum[slot][warp] = inc;
+  __syncthreads();  // every thread holds its words: the buffer may be refilled
+  if (tid == 0) {
+    const u64 gg = g + 2 * (u64)gridDim.x;
+    if (gg < gfull) dq_load_group(buf + slot * DQ_GWORDS, P.words + gg * DQ_GWORDS, DQ_GBYTES, &mbar[slot]);
+  }
+  u32 wpre = 0;
+#pragma unroll
+  for (int k = 0; k < DQ_NT / 32; ++k) wpre += (u32)k < warp ? wsum[slot][k] : 0u;
+  const u32 rel0 = wpre + inc - c;                 // ones of the CTA before this thread
+  const u64 b0t = w0 << 6;                         // this thread's first bit
+  const u32 vt = b0t < P.m ? (u32)min(P.m - b0t, (u64)(64 * DQ_WPT)) : 0u;  // its valid bits
+  // ---- lines, line samples, L2 entries ---------------------------------------
+  const bool full = vt == 64u * DQ_WPT;  // every bit valid (all but the level's last thread)
   {
-    const u64 w3 = ((u64)blockIdx.x * DQ_NT + tid) * 3;
+    u32 rel = rel0;
+    const u64 line0 = w0 / 3;
 #pragma unroll
-    for (int x = 0; x < 3; ++x) wn[x] = w3 + x < nw ? __ldg(P.words + w3 + x) : 0ull;
-  }
-  for (u64 g = blockIdx.x; g < ncta; g += gridDim.x) {
-    const u64 i = g * DQ_NT + tid;  // this thread's line
-    const u64 w3 = i * 3;
-    u64 w[3];
-#pragma unroll
-    for (int x = 0; x < 3; ++x) w[x] = wn[x];
-    {
-      const u64 w3n = (i + (u64)gridDim.x * DQ_NT) * 3;
-#pragma unroll
-      for (int x = 0; x < 3; ++x) wn[x] = w3n + x < nw ? __ldg(P.words + w3n + x) : 0ull;
-    }
-    const u64 cta1 = 3 * g < n_l1 ? __ldg(P.l1 + 3 * g) : total;  // ones before the CTA's first bit
-    u32 pc[3];
-#pragma unroll
-    for (int x = 0; x < 3; ++x) pc[x] = __popcll(w[x]);
-    const u32 c = pc[0] + pc[1] + pc[2];
-    u32 inc = c;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const u32 y = __shfl_up_sync(0xffffffffu, inc, d);
-      if (lane >= (u32)d) inc += y;
-    }
-    __syncthreads();  // wsum reuse
-    if (lane == 31) wsum[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-      u32 v = wsum[lane];
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const u32 y = __shfl_up_sync(0xffffffffu, v, d);
-        if (lane >= (u32)d) v += y;
+    for (int x = 0; x < DQ_LPT; ++x) {
+      const u64 i = line0 + x;
+      const u32 cl = pc[3 * x] + pc[3 * x + 1] + pc[3 * x + 2];
+      const u64 hdr = l1a + rel;
+      const u32 vl = full ? (u32)kQBits
+                          : vt > (u32)(kQBits * x) ? min(vt - (u32)(kQBits * x), (u32)kQBits) : 0u;
+      if (i < Q.n_lines) {
+        dq_store_line(Q.lines + i * kQLineU2, hdr, w[3 * x], w[3 * x + 1], w[3 * x + 2]);
+        dq_line_samples(Q.sel1, Q.cap1, hdr, cl, (u32)i);
+        if (vl) dq_line_samples(Q.sel0, Q.cap0, ((i * kQBits) - hdr), vl - cl, (u32)i);
       }
-      wsum[lane] = v;  // inclusive per warp
-    }
-    __syncthreads();
-    const u32 wpre = warp ? wsum[warp - 1] : 0u;
-    const u32 exl = inc - c;             // ones of the warp before this line
-    const u64 hdr = cta1 + wpre + exl;   // ones of the level before line i
-    const u64 b0 = i * kQBits;
-    if (i < Q.n_lines) {
-      ulonglong2* out = Q.lines + i * kQLineU2;
-      out[0] = make_ulonglong2(hdr, w[0]);
-      out[1] = make_ulonglong2(w[1], w[2]);
-      // line samples: line of every 2^kQSelLog-th one / zero
-      for (u64 j = (hdr + (1u << kQSelLog) - 1) >> kQSelLog; (j << kQSelLog) + 1 <= hdr + c; ++j)
-        if (j < Q.cap1) Q.sel1[j] = (u32)i;
-      if (b0 < P.m) {
-        const u64 valid = min(P.m - b0, (u64)kQBits);
-        const u64 zlo = b0 - hdr, zhi = zlo + (valid - c);
-        for (u64 j = (zlo + (1u << kQSelLog) - 1) >> kQSelLog; (j << kQSelLog) + 1 <= zhi; ++j)
-          if (j < Q.cap0) Q.sel0[j] = (u32)i;
-      }
-      // L2 entries of the line's words
-      u64 pre = hdr;
+      // L2 entries (3072 words per CTA: a multiple of every L2 block size)
+      u32 pre = rel;
 #pragma unroll
-      for (int x = 0; x < 3; ++x) {
-        const u64 wx = w3 + x;
-        if (wx < nw && ((u32)wx & l2m) == 0)
-          P.l2[(wx << 6) >> P.l2_log] = (u16)(pre - __ldg(P.l1 + (wx >> 10)));
-        pre += pc[x];
-      }
-    }
-    // reference samples: ordinals of the warp's range, owner by range
-    const u32 vl = b0 < P.m ? (u32)min(P.m - b0, (u64)kQBits) : 0u;  // the line's valid bits
-    const u64 zb = (b0 < P.m ? b0 : P.m) - hdr;                     // zeros before the line
-    const u32 zl = vl - c;
-#pragma unroll
-    for (int kind = 0; kind < 2; ++kind) {
-      const bool ones = kind == 0;
-      const u64 bl = ones ? hdr : zb;
-      const u32 cl = ones ? c : zl;
-      const u64 bw = __shfl_sync(0xffffffffu, bl, 0);
-      const u64 ew = __shfl_sync(0xffffffffu, bl + cl, 31);
-      for (u64 qo = dq_next_multiple(bw, P.rate, P.rate_log); qo <= ew; qo += P.rate) {
-        if (bl < qo && qo <= bl + cl) {
-          u32 k = (u32)(qo - bl);
-          u32 cw[3];
-#pragma unroll
-          for (int x = 0; x < 3; ++x) {
-            const u32 vbx = vl > 64u * x ? min(64u, vl - 64u * x) : 0u;
-            cw[x] = ones ? pc[x] : vbx - pc[x];
-          }
-          const u32 j = k > cw[0] ? (k > cw[0] + cw[1] ? 2u : 1u) : 0u;
-          k -= j == 0 ? 0u : j == 1 ? cw[0] : cw[0] + cw[1];
-          const u64 wv = j == 0 ? w[0] : j == 1 ? w[1] : w[2];
-          const u32 vb = vl > 64u * j ? min(64u, vl - 64u * j) : 0u;
-          const u64 wm = (ones ? wv : ~wv) & (vb >= 64 ? ~0ull : (1ull << vb) - 1ull);
-          const u64 pos = ((w3 + j) << 6) + select_in_word64(wm, k);
-          const u64 si = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
-          u64* o = ones ? P.ones : P.zeros;
-          if (si < (ones ? P.ones_cap : P.zeros_cap)) o[si] = pos;
+      for (int y = 0; y < 3; ++y) {
+        const u32 lw = tid * DQ_WPT + 3 * x + y;  // word inside the CTA
+        if ((lw & l2m) == 0 && (full || w0 + 3 * x + y < nw)) {
+          const u32 blk = lw >> 10;
+          P.l2[(gw0 + lw) >> l2wl] = (u16)(pre - (blk == 0 ? 0u : blk == 1 ? d1 : d2));
         }
+        pre += pc[3 * x + y];
       }
+      rel += cl;
     }
   }
+  // ---- reference samples: each lane its own ordinals (at rate 4096 a lane
+  // holds at most one of each kind; ~three lanes of a warp hold one) ---------
+  const u64 hb = l1a + rel0;                     // ones before this thread
+  const u64 zbt = (b0t < P.m ? b0t : P.m) - hb;  // zeros before this thread
+#pragma unroll
+  for (int kind = 0; kind < 2; ++kind) {
+    const bool ones = kind == 0;
+    const u64 bl = ones ? hb : zbt;
+    const u32 cl = ones ? c : vt - c;
+    for (u64 qo = dq_next_multiple(bl, P.rate, P.rate_log); qo <= bl + cl; qo += P.rate) {
+      // word j holding ordinal k: k > (kind's count of words 0..i) for i < j
+      const u32 k = (u32)(qo - bl);
+      u32 j = 0, before = 0, acc = 0;
+#pragma unroll
+      for (int i = 0; i < DQ_WPT - 1; ++i) {
+        const u32 vb = full ? 64u : vt > 64u * i ? min(64u, vt - 64u * i) : 0u;
+        acc += ones ? pc[i] : vb - pc[i];
+        const bool past = k > acc;
+        j += past ? 1u : 0u;
+        before = past ? acc : before;
+      }
+      u64 wv = w[0];
+#pragma unroll
+      for (int i = 1; i < DQ_WPT; ++i) wv = j == (u32)i ? w[i] : wv;
+      const u32 vb = full ? 64u : vt > 64u * j ? min(64u, vt - 64u * j) : 0u;
+      wv = (ones ? wv : ~wv) & (vb >= 64 ? ~0ull : (1ull << vb) - 1ull);
+      const u64 pos = ((w0 + j) << 6) + select_in_word64(wv, k - before);
+      const u64 si = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
+      u64* o = ones ? P.ones : P.zeros;
+      if (si < (ones ? P.ones_cap : P.zeros_cap)) o[si] = pos;
+    }
+  }
+  }  // groups
 }
 
-cudaError_t launch_dirq(const DirQParams& p, int sms, cudaStream_t st) {
+cudaError_t launch_dirq(const DirQParams& p, int sms, cudaStream_t st, bool pdl) {
   if (!p.n_lines) return cudaSuccess;
-  const u64 ncta = (p.n_lines + DQ_NT - 1) / DQ_NT;
-  u64 blocks = ncta;
-  if (blocks > (u64)sms * 2) blocks = (u64)sms * 2;
-  dirq_kernel<<<(unsigned)blocks, DQ_NT, 0, st>>>(p);
-  return cudaGetLastError();
+  static std::atomic<int> per_sm_cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const bool dev_ok = dev >= 0 && dev < 64;
+  int per_sm = dev_ok ? per_sm_cache[dev].load(std::memory_order_acquire) : 0;
+  if (per_sm <= 0) {  // the shared-memory opt-in belongs to the device context
+    cudaError_t e = cudaFuncSetAttribute(dirq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DQ_SMEM);
+    if (e != cudaSuccess) return e;
+    per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dirq_kernel, DQ_NT, DQ_SMEM);
+    if (per_sm < 1) per_sm = 1;
+    if (dev_ok) per_sm_cache[dev].store(per_sm, std::memory_order_release);
+  }
+  const u64 ncta = (p.n_lines + DQ_LINES - 1) / DQ_LINES;
+  const u64 cap = (u64)sms * per_sm;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ncta < cap ? ncta : cap));
+  cfg.blockDim = dim3(DQ_NT);
+  cfg.dynamicSmemBytes = DQ_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, dirq_kernel, p);
 }
 
 cudaError_t launch_qlayout(const LevelDev& L, const u64* total, u32 l2_shift, ulonglong2* lines,

@@ -1777,70 +1777,65 @@ __global__ void __launch_bounds__(256) wcount0_kernel(const TIn* __restrict__ te
 }
 
 // one CTA: exclusive scan of per-L1-block counts -> the level's L1 directory
-// (ones before each 65536-bit block) and its total.  Counts are read as
-// uint4 quads, quad j of round r by thread j - 1024 r (coalesced), all rounds'
-// loads in flight at once; each round is a block scan of the quad sums, and
-// every thread stores its four entries as two 16-byte stores (the earlier
-// contiguous-run-per-thread layout stored at a 128-byte lane stride).
-// Counts are padded to a multiple of 4 with zeros by the caller's memset.
+// (ones before each 65536-bit block) and its total.  Thread t owns L1_QPT
+// consecutive uint4 quads of counts per round (a round covers 2^14 blocks = a
+// 2^30-bit level, so C2's levels take one round and ONE block scan: the
+// earlier quad-per-thread rounds paid two barriers per 4096 blocks); sums
+// inside a round fit 32 bits (2^14 blocks x 2^16 bits).  Counts are padded to
+// a multiple of 4 with zeros by the caller's memset.
+constexpr int L1_QPT = 4;
 __global__ void __launch_bounds__(1024) l1_scan_kernel(const u32* __restrict__ counts, u64 n_l1,
                                                        u64* __restrict__ l1, u64* __restrict__ total) {
-  __shared__ u64 wsum[32];
+  __shared__ u32 wsum[32];
+  // a programmatic dependent launched after this kernel (the previous level's
+  // directory pass) needs nothing from it: release it at once
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u64 quads = (n_l1 + 3) / 4;
-  const u64 rounds = (quads + 1023) / 1024;
   const uint4* c4 = reinterpret_cast<const uint4*>(counts);
-  constexpr int RR = 8;  // rounds kept in registers (2^15 L1 blocks)
-  uint4 rv[RR];
-#pragma unroll
-  for (int r = 0; r < RR; ++r) {
-    const u64 q = (u64)r * 1024 + tid;
-    rv[r] = (u64)r < rounds && q < quads ? __ldg(c4 + q) : make_uint4(0, 0, 0, 0);
-  }
   u64 carry = 0;
-  for (u64 r = 0; r < rounds; ++r) {
-    const u64 q = r * 1024 + tid;
-    uint4 v;
-    if (r < (u64)RR) {
-      v = rv[0];
+  for (u64 base = 0; base < quads; base += 1024 * L1_QPT) {
+    uint4 v[L1_QPT];
+    u32 s = 0;
 #pragma unroll
-      for (int j = 1; j < RR; ++j) v = (u64)j == r ? rv[j] : v;
-    } else {
-      v = q < quads ? __ldg(c4 + q) : make_uint4(0, 0, 0, 0);
+    for (int j = 0; j < L1_QPT; ++j) {
+      const u64 q = base + (u64)tid * L1_QPT + j;
+      v[j] = q < quads ? __ldg(c4 + q) : make_uint4(0, 0, 0, 0);
+      s += v[j].x + v[j].y + v[j].z + v[j].w;
     }
-    const u64 sq = (u64)v.x + v.y + v.z + v.w;
-    u64 inc = sq;
+    u32 inc = s;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const u64 y = __shfl_up_sync(FULLM, inc, d);
+      const u32 y = __shfl_up_sync(FULLM, inc, d);
       if (lane >= d) inc += y;
     }
-    __syncthreads();  // wsum reuse across rounds
     if (lane == 31) wsum[warp] = inc;
     __syncthreads();
-    if (warp == 0) {
-      u64 t = wsum[lane];
+    u32 ws = wsum[lane];
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const u64 y = __shfl_up_sync(FULLM, t, d);
-        if (lane >= d) t += y;
-      }
-      wsum[lane] = t;
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 y = __shfl_up_sync(FULLM, ws, d);
+      if (lane >= d) ws += y;
     }
-    __syncthreads();
-    const u64 ex = carry + (warp ? wsum[warp - 1] : 0) + inc - sq;
-    if (q < quads) {
-      const u64 e0 = ex, e1 = e0 + v.x, e2 = e1 + v.y, e3 = e2 + v.z;
+    const u32 round_total = __shfl_sync(FULLM, ws, 31);
+    const u32 wpre = __shfl_sync(FULLM, ws - wsum[lane], warp);
+    u64 e = carry + wpre + (inc - s);
+#pragma unroll
+    for (int j = 0; j < L1_QPT; ++j) {
+      const u64 q = base + (u64)tid * L1_QPT + j;
+      const u64 e0 = e, e1 = e0 + v[j].x, e2 = e1 + v[j].y, e3 = e2 + v[j].z;
+      e = e3 + v[j].w;
       if (q * 4 + 3 < n_l1) {
         reinterpret_cast<ulonglong2*>(l1)[q * 2] = make_ulonglong2(e0, e1);
         reinterpret_cast<ulonglong2*>(l1)[q * 2 + 1] = make_ulonglong2(e2, e3);
-      } else {
+      } else if (q < quads) {
         const u64 ev[4] = {e0, e1, e2, e3};
         for (int i = 0; i < 4; ++i)
           if (q * 4 + i < n_l1) l1[q * 4 + i] = ev[i];
       }
     }
-    carry += wsum[31];
+    carry += round_total;
+    __syncthreads();  // wsum reuse
   }
   if (tid == 0) *total = carry;
 }

@@ -318,10 +318,15 @@ static void fill_treedev(wt_tree* t) {
 }
 
 // allocate the per-level directories and upload the O(sigma) tables
-static int alloc_tree(wt_tree* t, cudaStream_t st) {
+// Device arrays of a tree.  The build path splits this so the GPU never waits
+// on the host: alloc_tree_core (bit array, node table) before level 0,
+// alloc_level(l) inside the level loop (stream-ordered allocations the host
+// makes while earlier levels run), alloc_query_tables after the last launch
+// (its uploads run on a side stream from pinned staging, overlapping the
+// levels).  alloc_tree does all three synchronously (load / replicate).
+static int alloc_tree_core(wt_tree* t, cudaStream_t st) {
   const Plan& P = t->plan;
   t->lv.assign(P.L, LevelHost{});
-  TRY(dalloc(&t->words, P.n_words, st));
   for (uint32_t l = 0; l < P.L; ++l) {
     LevelHost& h = t->lv[l];
     const uint64_t m = (uint64_t)P.sizes[l];
@@ -329,46 +334,120 @@ static int alloc_tree(wt_tree* t, cudaStream_t st) {
     h.meta.n_l1 = (m + kL1Bits - 1) / kL1Bits;
     h.meta.n_l2 = (m + t->meta.l2_bits - 1) / t->meta.l2_bits;
     h.meta.n_nodes = P.n_nodes[l];
-    TRY(dalloc(&h.l1, h.meta.n_l1, st));
-    TRY(dalloc(&h.l2, h.meta.n_l2, st));
-    TRY(dalloc(&h.ones, m / t->meta.sample_rate, st));
-    TRY(dalloc(&h.zeros, m / t->meta.sample_rate, st));
     h.n_lines = qlayout_lines(m);
     h.sel_cap = (m >> kQSelLog) + 2;
-    TRY(dalloc(&h.lines, h.n_lines * kQLineU2, st));
-    TRY(dalloc(&h.sel1, h.sel_cap, st));
-    TRY(dalloc(&h.sel0, h.sel_cap, st));
   }
+  TRY(dalloc(&t->words, P.n_words, st));
   TRY(dalloc(&t->nodes, P.nodes.size(), st));
-  TRY(dalloc(&t->id_code, P.sigma, st));
-  TRY(dalloc(&t->cum, P.sigma + 1, st));
-  TRY(dalloc(&t->symbols, P.sigma, st));
-  TRY(dalloc(&t->sym2id, 65536, st));
-  TRY(dalloc(&t->bad, 1, st));
-  // host temporaries reused across builds (thread-local): freshly mapped
-  // pages cost ~0.5 ms of page faults per 2^16-symbol build
-  static thread_local std::vector<int> s2i;
-  s2i.assign(65536, -1);
-  for (uint32_t i = 0; i < P.sigma; ++i) s2i[P.symbols[i]] = (int)i;
-  CU(cudaMemcpyAsync(t->sym2id, s2i.data(), 65536 * 4, cudaMemcpyHostToDevice, st));
-  std::vector<u32> idc(P.sigma);
-  for (uint32_t i = 0; i < P.sigma; ++i) idc[i] = P.values[i] | ((u32)P.lens[i] << 16);
+  // (pageable source: the call returns once the bytes are staged)
   if (!P.nodes.empty())
     CU(cudaMemcpyAsync(t->nodes, P.nodes.data(), P.nodes.size() * sizeof(NodeEnt),
                        cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(t->id_code, idc.data(), idc.size() * 4, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(t->cum, P.cum.data(), P.cum.size() * 8, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(t->symbols, P.symbols.data(), P.symbols.size() * 2, cudaMemcpyHostToDevice,
-                     st));
-  CU(cudaStreamSynchronize(st));  // host vectors above are temporaries
   uint64_t bytes = P.n_words * 8 + P.nodes.size() * sizeof(NodeEnt) + P.sigma * 14 + 8;
-  node_cache().swap(t->plan.nodes);  // the device holds the node table now
-  t->plan.nodes.clear();
   for (auto& h : t->lv)
     bytes += h.meta.n_l1 * 8 + h.meta.n_l2 * 2 + 2 * (h.meta.n_bits / t->meta.sample_rate) * 8 +
              h.n_lines * kQLineBytes + 2 * h.sel_cap * 4;
   t->meta.device_bytes = bytes;
   return WT_OK;
+}
+
+static int alloc_level(wt_tree* t, uint32_t l, cudaStream_t st) {
+  LevelHost& h = t->lv[l];
+  if (h.l1) return WT_OK;
+  const uint64_t m = h.meta.n_bits;
+  TRY(dalloc(&h.l1, h.meta.n_l1, st));
+  TRY(dalloc(&h.l2, h.meta.n_l2, st));
+  TRY(dalloc(&h.ones, m / t->meta.sample_rate, st));
+  TRY(dalloc(&h.zeros, m / t->meta.sample_rate, st));
+  TRY(dalloc(&h.lines, h.n_lines * kQLineU2, st));
+  TRY(dalloc(&h.sel1, h.sel_cap, st));
+  TRY(dalloc(&h.sel0, h.sel_cap, st));
+  return WT_OK;
+}
+
+// pinned host staging for the query-table uploads (thread-local, grows)
+static void* pinned_staging(size_t bytes) {
+  static thread_local void* p = nullptr;
+  static thread_local size_t cap = 0;
+  if (bytes > cap) {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    cap = bytes;
+  }
+  return p;
+}
+
+// query-side tables (symbol -> id, id -> code, cum_hist, symbols); with a
+// side stream the uploads run there (from pinned staging) and `st` waits for
+// them at its current end (or, given `join`, wherever the caller waits on the
+// returned event); without one they run on `st` and the call syncs.
+static int alloc_query_tables(wt_tree* t, cudaStream_t st, cudaStream_t side,
+                              cudaEvent_t* join = nullptr) {
+  const Plan& P = t->plan;
+  TRY(dalloc(&t->id_code, P.sigma, st));
+  TRY(dalloc(&t->cum, P.sigma + 1, st));
+  TRY(dalloc(&t->symbols, P.sigma, st));
+  TRY(dalloc(&t->sym2id, 65536, st));
+  TRY(dalloc(&t->bad, 1, st));
+  const size_t b_s2i = 65536 * 4, b_idc = (size_t)P.sigma * 4, b_cum = P.cum.size() * 8,
+               b_sym = P.symbols.size() * 2;
+  u8* stage = side ? (u8*)pinned_staging(b_s2i + b_idc + b_cum + b_sym) : nullptr;
+  static thread_local std::vector<u8> pageable;
+  if (!stage) {
+    side = nullptr;
+    pageable.resize(b_s2i + b_idc + b_cum + b_sym);
+    stage = pageable.data();
+  }
+  int* s2i = reinterpret_cast<int*>(stage);
+  for (uint32_t s = 0; s < 65536; ++s) s2i[s] = -1;
+  for (uint32_t i = 0; i < P.sigma; ++i) s2i[P.symbols[i]] = (int)i;
+  u32* idc = reinterpret_cast<u32*>(stage + b_s2i);
+  for (uint32_t i = 0; i < P.sigma; ++i) idc[i] = P.values[i] | ((u32)P.lens[i] << 16);
+  memcpy(stage + b_s2i + b_idc, P.cum.data(), b_cum);
+  memcpy(stage + b_s2i + b_idc + b_cum, P.symbols.data(), b_sym);
+  cudaStream_t cs = side ? side : st;
+  cudaEvent_t ready = nullptr, done = nullptr;
+  if (side) {  // the side stream may touch the allocations once `st` reaches them
+    CU(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    CU(cudaEventRecord(ready, st));
+    CU(cudaStreamWaitEvent(side, ready, 0));
+  }
+  CU(cudaMemcpyAsync(t->sym2id, s2i, b_s2i, cudaMemcpyHostToDevice, cs));
+  CU(cudaMemcpyAsync(t->id_code, idc, b_idc, cudaMemcpyHostToDevice, cs));
+  CU(cudaMemcpyAsync(t->cum, stage + b_s2i + b_idc, b_cum, cudaMemcpyHostToDevice, cs));
+  CU(cudaMemcpyAsync(t->symbols, stage + b_s2i + b_idc + b_cum, b_sym, cudaMemcpyHostToDevice, cs));
+  if (side) {
+    CU(cudaEventRecord(done, side));
+    cudaEventDestroy(ready);
+    if (join) {  // the caller joins `st` to the uploads later
+      *join = done;
+    } else {
+      CU(cudaStreamWaitEvent(st, done, 0));
+      cudaEventDestroy(done);
+    }
+  } else {
+    CU(cudaStreamSynchronize(st));  // pageable staging is reused by the next call
+  }
+  return WT_OK;
+}
+
+static int finish_tables(wt_tree* t) {
+  node_cache().swap(t->plan.nodes);  // the device holds the node table now
+  t->plan.nodes.clear();
+  return WT_OK;
+}
+
+static int alloc_tree(wt_tree* t, cudaStream_t st) {
+  TRY(alloc_tree_core(t, st));
+  for (uint32_t l = 0; l < t->plan.L; ++l) TRY(alloc_level(t, l, st));
+  TRY(alloc_query_tables(t, st, nullptr));
+  return finish_tables(t);
 }
 
 // query-side layout of every level; totals_dev[l] = ones of level l (device)
@@ -603,8 +682,24 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       if (cudaMallocAsync(&probe, est, st) == cudaSuccess) cudaFreeAsync(probe, st);
       else cudaGetLastError();
     }
-    TRY(alloc_tree(t, st));
+    TRY(alloc_tree_core(t, st));
     tr.mark("tree allocated");
+    // query tables: uploads on a side stream (pinned staging) once level 0 is
+    // queued, so they overlap the levels; `st` joins them at its end
+    bool tables_done = false;
+    cudaEvent_t tables_join = nullptr;
+    struct JoinGuard { cudaEvent_t& e; ~JoinGuard() { if (e) cudaEventDestroy(e); } } jg{tables_join};
+    auto query_tables = [&]() -> int {
+      cudaStream_t side = nullptr;
+      if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        side = nullptr;
+      }
+      const int qrc = alloc_query_tables(t, st, side, &tables_join);
+      if (side) cudaStreamDestroy(side);  // (released once its work is done)
+      tables_done = true;
+      return qrc;
+    };
 
     // raw symbol -> code LUT for level 0, unless the map is the identity
     static thread_local std::vector<u16> lut;
@@ -751,6 +846,7 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       // L1 directory of level lv from its per-L1-block counts (l1cnt[cidx])
       std::vector<char> scanned(P.L + 1, 0);
       auto scan_level = [&](uint32_t lv, int cidx) -> int {
+        TRY(alloc_level(t, lv, st));
         LevelHost& hs = t->lv[lv];
         CU(launch_l1_scan(l1cnt[cidx], hs.meta.n_l1, hs.l1, totals + lv, st));
         scanned[lv] = 1;
@@ -758,11 +854,13 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       };
       int ci = 0;
       for (uint32_t l = 0; l < P.L; ++l) {
+        if (l == 1 && !tables_done) TRY(query_tables());  // level 0 is queued: overlap it
         const uint64_t m = (uint64_t)P.sizes[l];
         CU(cudaEventRecord(lev[l], st));
         if (m == 0) continue;
         const int in_bytes = l == 0 ? sym_bytes : P.code_bytes;
         LevelHost& h = t->lv[l];
+        TRY(alloc_level(t, l, st));
         if (!scanned[l]) TRY(scan_level(l, ci));
         const bool pair = pair_ok && l + 2 == P.L && (uint64_t)P.sizes[l + 1] == m;
         const bool next_blk = !pair && l + 1 < P.L && blk[l] && blk[l + 1];
@@ -850,7 +948,11 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       // (the query-side layouts run after the last level: overlapping them
       // with the next level's kernel on a side stream measured slower)
     }
+    for (uint32_t l = 0; l < P.L; ++l) TRY(alloc_level(t, l, st));  // (levels with no bits)
     TRY(launch_qlayouts(t, totals, st, &q_done));
+    if (!tables_done) TRY(query_tables());
+    if (tables_join) CU(cudaStreamWaitEvent(st, tables_join, 0));
+    TRY(finish_tables(t));
     tr.mark("levels launched");
     if (P.L) CU(cudaEventRecord(lev[P.L], st));
     CU(cudaEventRecord(e1, st));

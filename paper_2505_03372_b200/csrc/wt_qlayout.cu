@@ -106,13 +106,15 @@ __device__ __forceinline__ void dq_store_line(ulonglong2* p, u64 a, u64 b, u64 c
 }
 
 // line samples of one kind: sel[j] = line for every j with j * 2^kQSelLog + 1
-// in (before, before + cnt] (at most three: cnt <= 192)
-__device__ __forceinline__ void dq_line_samples(u32* sel, u64 cap, u64 before, u32 cnt, u32 line) {
+// in (before, before + cnt] (at most three: cnt <= 192), staged in shared
+// memory as the CTA-local line at j - jbase (the CTA's first sample index)
+__device__ __forceinline__ void dq_line_samples(u16* ss, u64 jbase, u64 before, u32 cnt, u32 line) {
   const u64 j0 = (before + (1u << kQSelLog) - 1) >> kQSelLog;
   const u32 k = (u32)(((before + cnt + (1u << kQSelLog) - 1) >> kQSelLog) - j0);
+  const u32 o = (u32)(j0 - jbase);
 #pragma unroll
   for (u32 x = 0; x < 3; ++x)
-    if (x < k && j0 + x < cap) sel[j0 + x] = line;
+    if (x < k) ss[o + x] = (u16)line;
 }
 
 __device__ __forceinline__ u32 dq_smem(const void* p) {
@@ -138,7 +140,8 @@ __device__ __forceinline__ void dq_wait(u64* bar, u32 parity) {
 
 constexpr int DQ_GWORDS = 3 * (kL1Bits / 64);  // words per CTA group (3072)
 constexpr int DQ_GBYTES = DQ_GWORDS * 8;       // 24 KiB
-constexpr int DQ_SMEM = 2 * DQ_GBYTES + 64;    // two group buffers + mbarriers
+constexpr int DQ_SSEL = DQ_GWORDS * 64 / (1 << kQSelLog) + 4;  // line samples of one kind per CTA
+constexpr int DQ_SMEM = 2 * DQ_GBYTES + 64 + 2 * DQ_SSEL * 2;  // group buffers, mbarriers, staged samples
 
 // Persistent: CTA b takes groups b, b + grid, ...; the next group's 24 KiB
 // stream into the other shared buffer by one bulk copy (cp.async.bulk +
@@ -150,6 +153,8 @@ __global__ void __launch_bounds__(DQ_NT, 3) dirq_kernel(const __grid_constant__ 
   extern __shared__ __align__(128) u8 dq_sm[];
   u64* buf = reinterpret_cast<u64*>(dq_sm);
   u64* mbar = reinterpret_cast<u64*>(dq_sm + 2 * DQ_GBYTES);
+  u16* ss1 = reinterpret_cast<u16*>(dq_sm + 2 * DQ_GBYTES + 64);  // staged line samples
+  u16* ss0 = ss1 + DQ_SSEL;
   __shared__ u32 wsum[2][DQ_NT / 32];
   const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u64 nw = (P.m + 63) >> 6;
@@ -209,12 +214,23 @@ __global__ void __launch_bounds__(DQ_NT, 3) dirq_kernel(const __grid_constant__ 
     const u64 gg = g + 2 * (u64)gridDim.x;
     if (gg < gfull) dq_load_group(buf + slot * DQ_GWORDS, P.words + gg * DQ_GWORDS, DQ_GBYTES, &mbar[slot]);
   }
-  u32 wpre = 0;
+  u32 wpre = 0, ctot = 0;
 #pragma unroll
-  for (int k = 0; k < DQ_NT / 32; ++k) wpre += (u32)k < warp ? wsum[slot][k] : 0u;
+  for (int k = 0; k < DQ_NT / 32; ++k) {
+    const u32 x = wsum[slot][k];
+    wpre += (u32)k < warp ? x : 0u;
+    ctot += x;
+  }
   const u32 rel0 = wpre + inc - c;                 // ones of the CTA before this thread
   const u64 b0t = w0 << 6;                         // this thread's first bit
   const u32 vt = b0t < P.m ? (u32)min(P.m - b0t, (u64)(64 * DQ_WPT)) : 0u;  // its valid bits
+  // the CTA's line samples: indices [jb1, je1) of sel1, [jb0, je0) of sel0
+  const u64 gb0 = gw0 << 6;
+  const u32 vg = gb0 < P.m ? (u32)min(P.m - gb0, (u64)DQ_GWORDS * 64) : 0u;  // the CTA's valid bits
+  const u64 zg = (gb0 < P.m ? gb0 : P.m) - l1a;                               // zeros before the CTA
+  constexpr u32 SR = (1u << kQSelLog) - 1;
+  const u64 jb1 = (l1a + SR) >> kQSelLog, je1 = (l1a + ctot + SR) >> kQSelLog;
+  const u64 jb0 = (zg + SR) >> kQSelLog, je0 = (zg + (vg - ctot) + SR) >> kQSelLog;
   // ---- lines, line samples, L2 entries ---------------------------------------
   const bool full = vt == 64u * DQ_WPT;  // every bit valid (all but the level's last thread)
   {
@@ -229,8 +245,8 @@ __global__ void __launch_bounds__(DQ_NT, 3) dirq_kernel(const __grid_constant__ 
                           : vt > (u32)(kQBits * x) ? min(vt - (u32)(kQBits * x), (u32)kQBits) : 0u;
       if (i < Q.n_lines) {
         dq_store_line(Q.lines + i * kQLineU2, hdr, w[3 * x], w[3 * x + 1], w[3 * x + 2]);
-        dq_line_samples(Q.sel1, Q.cap1, hdr, cl, (u32)i);
-        if (vl) dq_line_samples(Q.sel0, Q.cap0, ((i * kQBits) - hdr), vl - cl, (u32)i);
+        dq_line_samples(ss1, jb1, hdr, cl, (u32)(i - g * DQ_LINES));
+        if (vl) dq_line_samples(ss0, jb0, ((i * kQBits) - hdr), vl - cl, (u32)(i - g * DQ_LINES));
       }
       // L2 entries (3072 words per CTA: a multiple of every L2 block size)
       u32 pre = rel;
@@ -277,6 +293,16 @@ __global__ void __launch_bounds__(DQ_NT, 3) dirq_kernel(const __grid_constant__ 
       u64* o = ones ? P.ones : P.zeros;
       if (si < (ones ? P.ones_cap : P.zeros_cap)) o[si] = pos;
     }
+  }
+  // ---- the staged line samples leave coalesced -------------------------------
+  __syncthreads();
+  {
+    const u32 gl = (u32)(g * DQ_LINES);
+    const u32 n1 = (u32)(je1 - jb1), n0 = (u32)(je0 - jb0);
+    for (u32 x = tid; x < n1; x += DQ_NT)
+      if (jb1 + x < Q.cap1) Q.sel1[jb1 + x] = gl + ss1[x];
+    for (u32 x = tid; x < n0; x += DQ_NT)
+      if (jb0 + x < Q.cap0) Q.sel0[jb0 + x] = gl + ss0[x];
   }
   }  // groups
 }

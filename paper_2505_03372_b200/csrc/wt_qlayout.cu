@@ -108,10 +108,13 @@ __device__ __forceinline__ void dq_store_line(ulonglong2* p, u64 a, u64 b, u64 c
 // line samples of one kind: sel[j] = line for every j with j * 2^kQSelLog + 1
 // in (before, before + cnt] (at most three: cnt <= 192), staged in shared
 // memory as the CTA-local line at j - jbase (the CTA's first sample index)
-__device__ __forceinline__ void dq_line_samples(u16* ss, u64 jbase, u64 before, u32 cnt, u32 line) {
-  const u64 j0 = (before + (1u << kQSelLog) - 1) >> kQSelLog;
-  const u32 k = (u32)(((before + cnt + (1u << kQSelLog) - 1) >> kQSelLog) - j0);
-  const u32 o = (u32)(j0 - jbase);
+// (32-bit: `rb` = the CTA's count before the line + (count before the CTA
+// mod 2^kQSelLog), `ob` = (that residue + 2^kQSelLog - 1) >> kQSelLog)
+__device__ __forceinline__ void dq_line_samples(u16* ss, u32 ob, u32 rb, u32 cnt, u32 line) {
+  constexpr u32 SR = (1u << kQSelLog) - 1;
+  const u32 j0 = (rb + SR) >> kQSelLog;
+  const u32 k = ((rb + cnt + SR) >> kQSelLog) - j0;
+  const u32 o = j0 - ob;
 #pragma unroll
   for (u32 x = 0; x < 3; ++x)
     if (x < k) ss[o + x] = (u16)line;
@@ -143,59 +146,26 @@ constexpr int DQ_GBYTES = DQ_GWORDS * 8;       // 24 KiB
 constexpr int DQ_SSEL = DQ_GWORDS * 64 / (1 << kQSelLog) + 4;  // line samples of one kind per CTA
 constexpr int DQ_SMEM = 2 * DQ_GBYTES + 64 + 2 * DQ_SSEL * 2;  // group buffers, mbarriers, staged samples
 
-// Persistent: CTA b takes groups b, b + grid, ...; the next group's 24 KiB
-// stream into the other shared buffer by one bulk copy (cp.async.bulk +
-// mbarrier) while this one is processed, so each SM keeps ~100 KiB of reads in
-// flight without spending registers on them.  The level's partial last
-// group (its words end inside it) loads directly from global memory.
-__global__ void __launch_bounds__(DQ_NT, 3) dirq_kernel(const __grid_constant__ DirQParams Q) {
+// One group (CTA-local 32-bit arithmetic throughout).  FULL: every bit of the
+// group lies inside the level (all groups but the level's last), so no bound
+// checks.  The thread's words are in `w`; the group buffer `slot` may be
+// refilled once every thread holds its words (after the scan barrier).
+template <bool FULL>
+__device__ __forceinline__ void dq_group(const DirQParams& Q, const u64 (&w)[DQ_WPT], u64 g, u32 slot,
+                                         u32 (*wsum)[DQ_NT / 32], u16* ss1, u16* ss0, u64* buf,
+                                         u64* mbar, u64 gfull, u64 total) {
   const DirParams& P = Q.d;
-  extern __shared__ __align__(128) u8 dq_sm[];
-  u64* buf = reinterpret_cast<u64*>(dq_sm);
-  u64* mbar = reinterpret_cast<u64*>(dq_sm + 2 * DQ_GBYTES);
-  u16* ss1 = reinterpret_cast<u16*>(dq_sm + 2 * DQ_GBYTES + 64);  // staged line samples
-  u16* ss0 = ss1 + DQ_SSEL;
-  __shared__ u32 wsum[2][DQ_NT / 32];
   const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const u64 nw = (P.m + 63) >> 6;
   const u64 n_l1 = (P.m + kL1Bits - 1) / kL1Bits;
   const u32 l2m = (u32)((1ull << P.l2_log) >> 6) - 1u;  // L2 block = l2m + 1 words (<= 1024)
   const u32 l2wl = P.l2_log - 6;
-  const u64 ng = (Q.n_lines + DQ_LINES - 1) / DQ_LINES;
-  const u64 gfull = nw / DQ_GWORDS;  // groups whose words all lie inside the level
-  const u64 total = *Q.total;
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(dq_smem(&mbar[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(dq_smem(&mbar[1])));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (u32 k = 0; k < 2; ++k) {
-      const u64 gg = blockIdx.x + (u64)k * gridDim.x;
-      if (gg < gfull) dq_load_group(buf + k * DQ_GWORDS, P.words + gg * DQ_GWORDS, DQ_GBYTES, &mbar[k]);
-    }
-  }
-  __syncthreads();
-  u32 it = 0;
-  for (u64 g = blockIdx.x; g < ng; g += gridDim.x, ++it) {
-  const u32 slot = it & 1u;
-  const u64 gw0 = g * DQ_GWORDS;                 // the CTA's first word
-  const u64 w0 = gw0 + (u64)tid * DQ_WPT;        // this thread's first word
-  u64 w[DQ_WPT];
-  if (g < gfull) {
-    dq_wait(&mbar[slot], (it >> 1) & 1u);
-    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(buf + slot * DQ_GWORDS + tid * DQ_WPT);
-#pragma unroll
-    for (int j = 0; j < DQ_WPT / 2; ++j) {
-      const ulonglong2 v = src[j];
-      w[2 * j] = v.x;
-      w[2 * j + 1] = v.y;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < DQ_WPT; ++j) w[j] = w0 + j < nw ? __ldg(P.words + w0 + j) : 0ull;  // padding bits are zero
-  }
-  const u64 l1a = 3 * g < n_l1 ? __ldg(P.l1 + 3 * g) : total;  // ones before the CTA
-  const u32 d1 = 3 * g + 1 < n_l1 ? (u32)(__ldg(P.l1 + 3 * g + 1) - l1a) : 0u;
-  const u32 d2 = 3 * g + 2 < n_l1 ? (u32)(__ldg(P.l1 + 3 * g + 2) - l1a) : 0u;
+  constexpr u32 SR = (1u << kQSelLog) - 1;
+  const u64 gw0 = g * DQ_GWORDS;           // the CTA's first word
+  const u64 w0 = gw0 + (u64)tid * DQ_WPT;  // this thread's first word
+  const u64 l1a = FULL || 3 * g < n_l1 ? __ldg(P.l1 + 3 * g) : total;  // ones before the CTA
+  const u32 d1 = FULL || 3 * g + 1 < n_l1 ? (u32)(__ldg(P.l1 + 3 * g + 1) - l1a) : 0u;
+  const u32 d2 = FULL || 3 * g + 2 < n_l1 ? (u32)(__ldg(P.l1 + 3 * g + 2) - l1a) : 0u;
   u32 pc[DQ_WPT], c = 0;
 #pragma unroll
   for (int j = 0; j < DQ_WPT; ++j) {
@@ -221,39 +191,37 @@ __global__ void __launch_bounds__(DQ_NT, 3) dirq_kernel(const __grid_constant__ 
     wpre += (u32)k < warp ? x : 0u;
     ctot += x;
   }
-  const u32 rel0 = wpre + inc - c;                 // ones of the CTA before this thread
-  const u64 b0t = w0 << 6;                         // this thread's first bit
-  const u32 vt = b0t < P.m ? (u32)min(P.m - b0t, (u64)(64 * DQ_WPT)) : 0u;  // its valid bits
-  // the CTA's line samples: indices [jb1, je1) of sel1, [jb0, je0) of sel0
+  const u32 rel0 = wpre + inc - c;  // ones of the CTA before this thread
   const u64 gb0 = gw0 << 6;
-  const u32 vg = gb0 < P.m ? (u32)min(P.m - gb0, (u64)DQ_GWORDS * 64) : 0u;  // the CTA's valid bits
-  const u64 zg = (gb0 < P.m ? gb0 : P.m) - l1a;                               // zeros before the CTA
-  constexpr u32 SR = (1u << kQSelLog) - 1;
-  const u64 jb1 = (l1a + SR) >> kQSelLog, je1 = (l1a + ctot + SR) >> kQSelLog;
-  const u64 jb0 = (zg + SR) >> kQSelLog, je0 = (zg + (vg - ctot) + SR) >> kQSelLog;
+  // valid bits of this thread / of the CTA
+  const u32 vt = FULL ? 64u * DQ_WPT : (w0 << 6) < P.m ? (u32)min(P.m - (w0 << 6), (u64)(64 * DQ_WPT)) : 0u;
+  const u32 vg = FULL ? 64u * DQ_GWORDS : gb0 < P.m ? (u32)min(P.m - gb0, (u64)DQ_GWORDS * 64) : 0u;
+  const u64 zg = (FULL || gb0 < P.m ? gb0 : P.m) - l1a;  // zeros before the CTA
+  // the CTA's line samples: indices [jb, jb + n) of sel1 / sel0; per line the
+  // 32-bit residue arithmetic of dq_line_samples
+  const u32 r1 = (u32)l1a & SR, r0 = (u32)zg & SR;
+  const u32 ob1 = (r1 + SR) >> kQSelLog, ob0 = (r0 + SR) >> kQSelLog;
   // ---- lines, line samples, L2 entries ---------------------------------------
-  const bool full = vt == 64u * DQ_WPT;  // every bit valid (all but the level's last thread)
   {
     u32 rel = rel0;
-    const u64 line0 = w0 / 3;
 #pragma unroll
     for (int x = 0; x < DQ_LPT; ++x) {
-      const u64 i = line0 + x;
+      const u32 li = tid * DQ_LPT + x;  // line inside the CTA
+      const u64 i = g * DQ_LINES + li;
       const u32 cl = pc[3 * x] + pc[3 * x + 1] + pc[3 * x + 2];
-      const u64 hdr = l1a + rel;
-      const u32 vl = full ? (u32)kQBits
+      const u32 vl = FULL ? (u32)kQBits
                           : vt > (u32)(kQBits * x) ? min(vt - (u32)(kQBits * x), (u32)kQBits) : 0u;
-      if (i < Q.n_lines) {
-        dq_store_line(Q.lines + i * kQLineU2, hdr, w[3 * x], w[3 * x + 1], w[3 * x + 2]);
-        dq_line_samples(ss1, jb1, hdr, cl, (u32)(i - g * DQ_LINES));
-        if (vl) dq_line_samples(ss0, jb0, ((i * kQBits) - hdr), vl - cl, (u32)(i - g * DQ_LINES));
+      if (FULL || i < Q.n_lines) {
+        dq_store_line(Q.lines + i * kQLineU2, l1a + rel, w[3 * x], w[3 * x + 1], w[3 * x + 2]);
+        dq_line_samples(ss1, ob1, r1 + rel, cl, li);
+        if (FULL || vl) dq_line_samples(ss0, ob0, r0 + (li * (u32)kQBits - rel), vl - cl, li);
       }
       // L2 entries (3072 words per CTA: a multiple of every L2 block size)
       u32 pre = rel;
 #pragma unroll
       for (int y = 0; y < 3; ++y) {
         const u32 lw = tid * DQ_WPT + 3 * x + y;  // word inside the CTA
-        if ((lw & l2m) == 0 && (full || w0 + 3 * x + y < nw)) {
+        if ((lw & l2m) == 0 && (FULL || w0 + 3 * x + y < nw)) {
           const u32 blk = lw >> 10;
           P.l2[(gw0 + lw) >> l2wl] = (u16)(pre - (blk == 0 ? 0u : blk == 1 ? d1 : d2));
         }
@@ -264,8 +232,8 @@ __global__ void __launch_bounds__(DQ_NT, 3) dirq_kernel(const __grid_constant__ 
   }
   // ---- reference samples: each lane its own ordinals (at rate 4096 a lane
   // holds at most one of each kind; ~three lanes of a warp hold one) ---------
-  const u64 hb = l1a + rel0;                     // ones before this thread
-  const u64 zbt = (b0t < P.m ? b0t : P.m) - hb;  // zeros before this thread
+  const u64 hb = l1a + rel0;                                      // ones before this thread
+  const u64 zbt = (FULL || (w0 << 6) < P.m ? (w0 << 6) : P.m) - hb;  // zeros before this thread
 #pragma unroll
   for (int kind = 0; kind < 2; ++kind) {
     const bool ones = kind == 0;
@@ -277,7 +245,7 @@ __global__ void __launch_bounds__(DQ_NT, 3) dirq_kernel(const __grid_constant__ 
       u32 j = 0, before = 0, acc = 0;
 #pragma unroll
       for (int i = 0; i < DQ_WPT - 1; ++i) {
-        const u32 vb = full ? 64u : vt > 64u * i ? min(64u, vt - 64u * i) : 0u;
+        const u32 vb = FULL ? 64u : vt > 64u * i ? min(64u, vt - 64u * i) : 0u;
         acc += ones ? pc[i] : vb - pc[i];
         const bool past = k > acc;
         j += past ? 1u : 0u;
@@ -286,7 +254,7 @@ __global__ void __launch_bounds__(DQ_NT, 3) dirq_kernel(const __grid_constant__ 
       u64 wv = w[0];
 #pragma unroll
       for (int i = 1; i < DQ_WPT; ++i) wv = j == (u32)i ? w[i] : wv;
-      const u32 vb = full ? 64u : vt > 64u * j ? min(64u, vt - 64u * j) : 0u;
+      const u32 vb = FULL ? 64u : vt > 64u * j ? min(64u, vt - 64u * j) : 0u;
       wv = (ones ? wv : ~wv) & (vb >= 64 ? ~0ull : (1ull << vb) - 1ull);
       const u64 pos = ((w0 + j) << 6) + select_in_word64(wv, k - before);
       const u64 si = (P.rate_log >= 0 ? (qo >> P.rate_log) : qo / P.rate) - 1;
@@ -294,17 +262,72 @@ __global__ void __launch_bounds__(DQ_NT, 3) dirq_kernel(const __grid_constant__ 
       if (si < (ones ? P.ones_cap : P.zeros_cap)) o[si] = pos;
     }
   }
-  // ---- the staged line samples leave coalesced -------------------------------
+  // ---- the staged line samples leave coalesced (sel_cap exceeds every index)
   __syncthreads();
   {
     const u32 gl = (u32)(g * DQ_LINES);
-    const u32 n1 = (u32)(je1 - jb1), n0 = (u32)(je0 - jb0);
-    for (u32 x = tid; x < n1; x += DQ_NT)
-      if (jb1 + x < Q.cap1) Q.sel1[jb1 + x] = gl + ss1[x];
-    for (u32 x = tid; x < n0; x += DQ_NT)
-      if (jb0 + x < Q.cap0) Q.sel0[jb0 + x] = gl + ss0[x];
+    const u64 jb1 = (l1a + SR) >> kQSelLog, jb0 = (zg + SR) >> kQSelLog;
+    const u32 n1 = (u32)(((l1a + ctot + SR) >> kQSelLog) - jb1);
+    const u32 n0 = (u32)(((zg + (vg - ctot) + SR) >> kQSelLog) - jb0);
+    u32* s1 = Q.sel1 + jb1;
+    u32* s0 = Q.sel0 + jb0;
+    for (u32 x = tid; x < n1; x += DQ_NT) s1[x] = gl + ss1[x];
+    for (u32 x = tid; x < n0; x += DQ_NT) s0[x] = gl + ss0[x];
   }
-  }  // groups
+}
+
+// Persistent: CTA b takes groups b, b + grid, ...; the next group's 24 KiB
+// stream into the other shared buffer by one bulk copy (cp.async.bulk +
+// mbarrier) while this one is processed, so each SM keeps ~100 KiB of reads in
+// flight without spending registers on them.  The level's partial last
+// group (its words end inside it) loads directly from global memory.
+__global__ void __launch_bounds__(DQ_NT, 3) dirq_kernel(const __grid_constant__ DirQParams Q) {
+  const DirParams& P = Q.d;
+  extern __shared__ __align__(128) u8 dq_sm[];
+  u64* buf = reinterpret_cast<u64*>(dq_sm);
+  u64* mbar = reinterpret_cast<u64*>(dq_sm + 2 * DQ_GBYTES);
+  u16* ss1 = reinterpret_cast<u16*>(dq_sm + 2 * DQ_GBYTES + 64);  // staged line samples
+  u16* ss0 = ss1 + DQ_SSEL;
+  __shared__ u32 wsum[2][DQ_NT / 32];
+  const u32 tid = threadIdx.x;
+  const u64 nw = (P.m + 63) >> 6;
+  const u64 ng = (Q.n_lines + DQ_LINES - 1) / DQ_LINES;
+  const u64 gfull = nw / DQ_GWORDS;                           // groups whose words all lie inside the level
+  const u64 gbits = P.m / ((u64)DQ_GWORDS * 64);              // groups whose bits all do
+  const u64 total = *Q.total;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(dq_smem(&mbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(dq_smem(&mbar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (u32 k = 0; k < 2; ++k) {
+      const u64 gg = blockIdx.x + (u64)k * gridDim.x;
+      if (gg < gfull) dq_load_group(buf + k * DQ_GWORDS, P.words + gg * DQ_GWORDS, DQ_GBYTES, &mbar[k]);
+    }
+  }
+  __syncthreads();
+  u32 it = 0;
+  for (u64 g = blockIdx.x; g < ng; g += gridDim.x, ++it) {
+    const u32 slot = it & 1u;
+    const u64 w0 = g * DQ_GWORDS + (u64)tid * DQ_WPT;  // this thread's first word
+    u64 w[DQ_WPT];
+    if (g < gfull) {
+      dq_wait(&mbar[slot], (it >> 1) & 1u);
+      const ulonglong2* src = reinterpret_cast<const ulonglong2*>(buf + slot * DQ_GWORDS + tid * DQ_WPT);
+#pragma unroll
+      for (int j = 0; j < DQ_WPT / 2; ++j) {
+        const ulonglong2 v = src[j];
+        w[2 * j] = v.x;
+        w[2 * j + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < DQ_WPT; ++j) w[j] = w0 + j < nw ? __ldg(P.words + w0 + j) : 0ull;  // padding bits are zero
+    }
+    if (g < gbits)
+      dq_group<true>(Q, w, g, slot, wsum, ss1, ss0, buf, mbar, gfull, total);
+    else
+      dq_group<false>(Q, w, g, slot, wsum, ss1, ss0, buf, mbar, gfull, total);
+  }
 }
 
 cudaError_t launch_dirq(const DirQParams& p, int sms, cudaStream_t st, bool pdl) {

@@ -2,8 +2,8 @@
 realistic size, for one `ncu --set full` capture of all of them
 (scripts/gpu_ncu_all.sh; summary: profiles/rNN_ncu_all_kernels.txt).
 
-  C2 build (u8, sigma=256, block mode)   hist8_blocks, block_l1, l1_scan, wlevel<u8,u8,1>, wpair, dir, qlayout
-  2^24 u8 builds                          wlevel tile mode, wcount0, dirq (WT_DIRQ=1)
+  C2 build (u8, sigma=256, block mode)   hist8_blocks, block_l1, l1_scan, wlevel<u8,u8,1>, wpair, dirq
+  2^24 u8 builds                          wlevel tile mode, wcount0; dir + qlayout (WT_DIRQ=0)
   u8 LUT build (sigma=200, 2^28)          hist8, wcount0, wlevel<u8,u8,lut>, wlast<lut>
   C3u-like build (u16, 2^28)              hist16p, hist16_fold, wlevel<u16,u16>
   declared alphabet with a stray symbol   first_outside
@@ -31,12 +31,12 @@ n = 1 << 30
 text = torch.randint(0, 256, (n,), generator=g, device=dev, dtype=torch.int32).to(torch.uint8)
 t = W.construct(text)
 del text
-# tile mode (2^24 symbols: too few L1 blocks for block mode) and the opt-in
-# one-pass directory + query layout (dirq_kernel)
+# tile mode (2^24 symbols: too few L1 blocks for block mode) and the split
+# directory (dir_kernel) + query layout (qlayout_kernel) path (WT_DIRQ=0)
 text = torch.randint(0, 256, (1 << 24,), generator=g, device=dev, dtype=torch.int32).to(torch.uint8)
 t24 = W.construct(text)
 del t24
-os.environ["WT_DIRQ"] = "1"
+os.environ["WT_DIRQ"] = "0"
 t24 = W.construct(text)
 del t24
 os.environ.pop("WT_DIRQ")

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 #include <dlfcn.h>
 #include <mutex>
 #include <string>
@@ -247,6 +248,7 @@ struct wt_tree {
   u16* symbols = nullptr;
   int* sym2id = nullptr;
   u64* bad = nullptr;  // first invalid query index (device scalar)
+  u8* arena = nullptr;  // every level's directory / line arrays (one allocation)
   TreeDev dev{};
   int rate_log = -1;
   cudaStream_t stream = nullptr;
@@ -338,6 +340,34 @@ static int alloc_tree_core(wt_tree* t, cudaStream_t st) {
     h.sel_cap = (m >> kQSelLog) + 2;
   }
   TRY(dalloc(&t->words, P.n_words, st));
+  // every level's directory / line arrays carved from ONE allocation: one
+  // stream-ordered allocation call instead of seven per level, and the same
+  // pool footprint build after build
+  {
+    auto al = [](uint64_t b) { return (b + 255) & ~255ull; };
+    uint64_t need = 0;
+    for (auto& h : t->lv) {
+      const uint64_t m = h.meta.n_bits, ns = m / t->meta.sample_rate;
+      need += al(h.meta.n_l1 * 8) + al(h.meta.n_l2 * 2) + 2 * al(std::max<uint64_t>(ns, 1) * 8) +
+              al(h.n_lines * kQLineBytes) + 2 * al(h.sel_cap * 4);
+    }
+    TRY(dalloc(&t->arena, std::max<uint64_t>(need, 1), st));
+    uint64_t o = 0;
+    auto take = [&](auto*& p, uint64_t bytes) {
+      p = reinterpret_cast<std::remove_reference_t<decltype(p)>>(t->arena + o);
+      o += al(bytes);
+    };
+    for (auto& h : t->lv) {
+      const uint64_t m = h.meta.n_bits, ns = m / t->meta.sample_rate;
+      take(h.l1, h.meta.n_l1 * 8);
+      take(h.l2, h.meta.n_l2 * 2);
+      take(h.ones, std::max<uint64_t>(ns, 1) * 8);
+      take(h.zeros, std::max<uint64_t>(ns, 1) * 8);
+      take(h.lines, h.n_lines * kQLineBytes);
+      take(h.sel1, h.sel_cap * 4);
+      take(h.sel0, h.sel_cap * 4);
+    }
+  }
   TRY(dalloc(&t->nodes, P.nodes.size(), st));
   // (pageable source: the call returns once the bytes are staged)
   if (!P.nodes.empty())
@@ -497,13 +527,15 @@ static void free_tree_arrays(wt_tree* t) {
   };
   F(t->words);
   for (auto& h : t->lv) {
-    F(h.l1);
-    F(h.l2);
-    F(h.ones);
-    F(h.zeros);
-    F(h.lines);
-    F(h.sel1);
-    F(h.sel0);
+    if (!t->arena) {  // (carved from the arena otherwise)
+      F(h.l1);
+      F(h.l2);
+      F(h.ones);
+      F(h.zeros);
+      F(h.lines);
+      F(h.sel1);
+      F(h.sel0);
+    }
   }
   F(t->nodes);
   F(t->id_code);
@@ -511,6 +543,7 @@ static void free_tree_arrays(wt_tree* t) {
   F(t->symbols);
   F(t->sym2id);
   F(t->bad);
+  F(t->arena);
   F(t->qbuf[0]);
   F(t->qbuf[1]);
   for (auto& s : t->qstream)

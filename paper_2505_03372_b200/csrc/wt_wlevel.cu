@@ -42,7 +42,7 @@ namespace {
 constexpr int W_NT = 128;
 constexpr int W_WARPS = W_NT / 32;
 #ifndef WT_W_RING
-#define WT_W_RING 2
+#define WT_W_RING 1
 #endif
 constexpr int W_RING = WT_W_RING;  // input tiles in flight per warp
 #ifndef WT_W_NSTAGE
@@ -54,7 +54,7 @@ constexpr int W_NSTAGE = WT_W_NSTAGE;  // staging buffers per warp (1 | 2)
 #endif
 constexpr int W_MINB = WT_W_MINB;  // __launch_bounds__ min CTAs per SM
 #ifndef WT_W_MINB4
-#define WT_W_MINB4 4
+#define WT_W_MINB4 6
 #endif
 constexpr int W_MINB4 = WT_W_MINB4;  // the same for 4 KiB tiles (u8 input)
 #ifndef WT_SAG
@@ -659,7 +659,7 @@ __device__ __forceinline__ void wpair_bits(const u8* stage, u32 cnt, u32 soff, u
 // pass 1 (the staged runs are re-read only for a run crossing an L1 block);
 // 2 (kPair): the next level is the last, its bits written from the staging.
 template <typename TIn, typename TC, bool kLut, int MODE>
-__global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? W_MINB4 : W_MINB)  // 4 KiB tiles: smem allows 4 CTAs
+__global__ void __launch_bounds__(W_NT, WS<TIn>::BYTES > 2048 ? W_MINB4 : W_MINB)  // one 4 KiB ring slot per warp: 6 CTAs (80 registers; measured faster than 4 CTAs with two slots)
     wlevel_kernel(const __grid_constant__ WLevelParams P) {
   constexpr bool kPair = MODE == 2, kBlk = MODE == 1;
   using S = WS<TIn>;
@@ -1461,8 +1461,11 @@ __device__ __forceinline__ u32 wp_gather(u32 f0, u32 f1) {
   return (((f1 * 16u + f0) * 0x01020408u) >> 24) & 0xffu;
 }
 
+#ifndef WP_MINB
+#define WP_MINB 3
+#endif
 template <typename TIn, typename TC, bool kLut>
-__global__ void __launch_bounds__(256, 2) wpair_kernel(const __grid_constant__ WLevelParams P) {
+__global__ void __launch_bounds__(256, WP_MINB) wpair_kernel(const __grid_constant__ WLevelParams P) {
   using S = WS<TIn>;
   constexpr int TILE = S::TILE, TPL1 = S::TPL1, TB = S::BYTES;
   constexpr int K = S::K;                    // 16-byte chunks per lane (8)

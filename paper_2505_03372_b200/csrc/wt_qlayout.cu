@@ -281,7 +281,10 @@ __device__ __forceinline__ void dq_group(const DirQParams& Q, const u64 (&w)[DQ_
 // mbarrier) while this one is processed, so each SM keeps ~100 KiB of reads in
 // flight without spending registers on them.  The level's partial last
 // group (its words end inside it) loads directly from global memory.
-__global__ void __launch_bounds__(DQ_NT, 3) dirq_kernel(const __grid_constant__ DirQParams Q) {
+#ifndef DQ_MINB
+#define DQ_MINB 3
+#endif
+__global__ void __launch_bounds__(DQ_NT, DQ_MINB) dirq_kernel(const __grid_constant__ DirQParams Q) {
   const DirParams& P = Q.d;
   extern __shared__ __align__(128) u8 dq_sm[];
   u64* buf = reinterpret_cast<u64*>(dq_sm);

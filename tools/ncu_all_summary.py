@@ -89,7 +89,7 @@ def main(path, peak):
 
 
 if __name__ == "__main__":
-    peak = float(sys.argv[2]) if len(sys.argv) > 2 else json.load(
+    peak = float(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] else json.load(
         open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                           "MEASURED_PEAKS.json")))["hbm_gbs"]
     main(sys.argv[1], peak)

@@ -142,12 +142,19 @@ __global__ void __launch_bounds__(H16_NT, 1) hist16p_kernel(const u16* __restric
   };
   const u64 nvec = n >> 3;
   const u64 stride = (u64)gridDim.x * H16_NT;
-  // warp-uniform trip count (the per-block reduction below needs every lane)
-  for (u64 wv = (u64)blockIdx.x * H16_NT + (tid & ~31); wv < nvec; wv += stride) {
+  // warp-uniform trip count (the per-block reduction below needs every lane);
+  // the next iteration's 16 bytes are loaded before this one's counters are
+  // bumped (one CTA per SM: without the prefetch each thread had one load in
+  // flight, 16 KiB per SM -- far too little to cover HBM latency)
+  const uint4* t4 = reinterpret_cast<const uint4*>(text);
+  u64 wv = (u64)blockIdx.x * H16_NT + (tid & ~31);
+  uint4 qn = make_uint4(0, 0, 0, 0);
+  if (wv + (tid & 31) < nvec) qn = __ldg(t4 + wv + (tid & 31));
+  for (; wv < nvec; wv += stride) {
     const u64 v = wv + (tid & 31);
-    uint4 q = make_uint4(0, 0, 0, 0);
+    uint4 q = qn;
+    qn = wv + stride + (tid & 31) < nvec ? __ldg(t4 + wv + stride + (tid & 31)) : make_uint4(0, 0, 0, 0);
     if (v < nvec) {
-      q = __ldg(reinterpret_cast<const uint4*>(text) + v);
       const u32 w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {

@@ -10,7 +10,7 @@
 // elements) and never waits for another warp: no __syncthreads in the loop.
 // Per tile:
 //   0. the tile streams into a per-warp shared-memory ring (cp.async.bulk +
-//      mbarrier) two tiles ahead;
+//      mbarrier), W_RING tiles ahead (one: 6 CTAs per SM fit);
 //   1. lane rows: a tile is 16 (u8) / 8 (u16) rows of 256 elements, lane i
 //      owns elements [8i, 8i + 8) of each row; one 8-bit mask per lane-row
 //      (SWAR bit extraction, or `symbol >= thr` at a LUT level 0), packed warp
@@ -214,6 +214,10 @@ __device__ __forceinline__ u64 wnext_multiple(u64 o, u64 rate, int rate_log) {
 // spanning several nodes): loads from global memory, element-by-element
 // destination stores, per-element next-level counts.
 // returns the tile's ones (block mode: the caller's running count)
+#ifndef WT_GT_UNROLL
+#define WT_GT_UNROLL 1
+#endif
+constexpr int kGtUnroll = WT_GT_UNROLL;  // general_tile's per-element loop
 template <typename TIn, typename TC, bool kLut, int MODE>
 __device__ __noinline__ u32 general_tile(const WLevelParams& P, u32 t, const u16* slut, u64 p1_in) {
   constexpr bool kPair = MODE == 2, kBlk = MODE == 1;
@@ -357,11 +361,14 @@ __device__ __noinline__ u32 general_tile(const WLevelParams& P, u32 t, const u16
     {
       TC* gout = reinterpret_cast<TC*>(P.out);
       const u32 sh1 = P.shift_bit - 1;
-#pragma unroll
+      // (rolled loops: this path is rare on most levels, but where tiles
+      // span many nodes -- Zipf texts, deep u16 levels -- the unrolled body
+      // thrashed the instruction cache: ncu `no_instructions` 52 %)
+#pragma unroll 1
       for (int k = 0; k < S::K; ++k) {
         const u32 e = (u32)(k * 32 + lane) * CH;
         u32 r1 = r1c[k];
-#pragma unroll
+#pragma unroll(kGtUnroll)
         for (int j = 0; j < CH; ++j) {
           // next-level ones, warp-aggregated per destination tile: lanes
           // whose element lands in the same next-level tile add together

@@ -270,15 +270,19 @@ def _build_timed(W, text_dev, alpha, steps, warmup):
         lvl.append([prof[i] for i in range(1 + tree.num_levels)])
         if s < steps - 1:
             del tree
-    return tree, ms, np.mean(np.array(lvl), axis=0)
+    return tree, ms, np.median(np.array(lvl), axis=0)
 
 
 def _build_record(tree, n, w, ms, lvl, hbm):
     sizes = [int(x) for x in tree.level_sizes]
     c = 1 if tree.num_levels <= 8 else 2
-    t_ms = float(np.mean(ms))
+    # median over the timed builds: one build whose pre-phase waited on a
+    # host-side stall (seen once at 130 ms in a C3z pre-phase) would otherwise
+    # set the figure; the mean and the minimum are reported beside it
+    t_ms = float(np.median(ms))
     alg = build_alg_bytes(sizes, n, w, c)
     rec = {"symbols_per_s": n / (t_ms / 1e3), "ms": t_ms, "ms_min": float(np.min(ms)),
+           "ms_mean": float(np.mean(ms)), "ms_all": [float(x) for x in ms],
            "GB_per_s": alg / (t_ms / 1e3) / 1e9, "alg_bytes": alg,
            "frac_of_hbm": alg / (t_ms / 1e3) / 1e9 / hbm, "n": n, "sigma": tree.sigma,
            "levels": tree.num_levels, "ms_histogram_and_plan": float(lvl[0]),
@@ -555,11 +559,16 @@ def run_ours(args):
         assert np.array_equal(ra, B.out["access"].cpu().numpy())
         assert np.array_equal(rr, B.out["rank"].cpu().numpy())
         assert np.array_equal(rs, B.out["select"].cpu().numpy())
+        # h2d bytes as the pipeline copied them (narrow wire: u32 arguments +
+        # u16 symbols packed on the host); the API's own int64 inputs beside it
         e2e = {"value": world * m_total / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": int(per[0] * 8 + (per[1] + per[2]) * 16),
+               "h2d_bytes_per_step": int(sum(runners[k].h2d_bytes for k in KINDS)),
+               "api_input_bytes_per_step": int(per[0] * 8 + (per[1] + per[2]) * 16),
+               "narrow_chunks": {k: [runners[k].narrow_chunks, runners[k].chunks] for k in KINDS},
                "d2h_bytes_per_step": int(per[0] * 1 + (per[1] + per[2]) * 8),
                "api": "BatchRunner(sort=True).run (access_batch / rank_batch / select_batch) "
-                      "on pinned numpy arrays, chunk 2^21",
+                      "on pinned numpy arrays, chunk 2^21; int64 inputs packed to the "
+                      "narrow wire (u16 symbols, u32 arguments) by a host thread pool",
                "per_kind": {k: {"ms": kind_s[k] * 1e3 / args.steps,
                                 "stage_ms": runners[k].stage_seconds * 1e3,
                                 "process_ms": runners[k].process_seconds * 1e3,

@@ -191,6 +191,10 @@ typedef struct {
     float kernel_ms;         /* sum of kernel durations                     */
     float d2h_ms;            /* last kernel end -> last copy-out end         */
     float total_ms;          /* first copy-in start -> last copy-out end     */
+    uint64_t h2d_bytes;      /* bytes copied host->device (narrow wire: 6 per
+                                rank / select query, 4 per access query;
+                                16 / 8 for chunks that crossed wide)         */
+    uint64_t narrow_chunks;  /* chunks that crossed on the narrow wire       */
 } wt_query_stats;
 /* wt_tree_query plus the pipeline accounting (stats may be NULL).          */
 int wt_tree_query_ex(wt_tree* t, int kind, const int64_t* ids, const int64_t* args,

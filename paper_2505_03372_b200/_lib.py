@@ -51,7 +51,8 @@ class QueryStats(C.Structure):
     """wt_query_stats (include/wt_b200.h): the host pipeline's accounting."""
     _fields_ = [("chunks", C.c_uint64), ("slots", C.c_uint64), ("chunk_records", C.c_uint64),
                 ("peak_records", C.c_uint64), ("h2d_ms", C.c_float), ("kernel_ms", C.c_float),
-                ("d2h_ms", C.c_float), ("total_ms", C.c_float)]
+                ("d2h_ms", C.c_float), ("total_ms", C.c_float), ("h2d_bytes", C.c_uint64),
+                ("narrow_chunks", C.c_uint64)]
 
 
 _vp, _u64, _u32, _i32, _f32p = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(C.c_float)

@@ -86,6 +86,8 @@ class BatchRunner:
         self.staging_allocated_records = 0
         self.staging_peak_records = 0
         self.stage_seconds = 0.0     # host->device copies of the chunks (device time)
+        self.h2d_bytes = 0           # bytes copied host->device by the last run
+        self.narrow_chunks = 0       # its chunks that crossed on the narrow wire
         self.process_seconds = 0.0   # query kernels (device time)
         self.unstage_seconds = 0.0   # kernel end -> results copied back
         self.wall_seconds = 0.0
@@ -108,6 +110,8 @@ class BatchRunner:
     def run(self, batch: QueryBatch) -> np.ndarray:
         nq = len(batch)
         tree = self.tree
+        self.h2d_bytes = 0
+        self.narrow_chunks = 0
         self.stage_seconds = 0.0
         self.process_seconds = 0.0
         if nq == 0:
@@ -132,6 +136,8 @@ class BatchRunner:
         self.staging_allocated_records = int(st.slots * st.chunk_records)
         self.staging_peak_records = int(st.peak_records)
         self.chunks = int(st.chunks)
+        self.h2d_bytes = int(st.h2d_bytes)          # as copied (narrow wire: 6 / 4 B per query)
+        self.narrow_chunks = int(st.narrow_chunks)
         if bad >= 0:
             raise BatchError(bad, self._cause(batch, bad))
         return out

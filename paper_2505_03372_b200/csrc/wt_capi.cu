@@ -7,7 +7,12 @@
 #include <cstring>
 #include <type_traits>
 #include <dlfcn.h>
+#include <atomic>
+#include <immintrin.h>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -258,6 +263,11 @@ struct wt_tree {
   cudaStream_t qstream[3] = {nullptr, nullptr, nullptr};  // copy-in, compute, copy-out
   cudaEvent_t qev[3][2] = {};                              // per stage and slot
   std::vector<cudaEvent_t> tev;                            // pipeline timing events (stats)
+  // narrow wire format: pinned host staging per slot (u32 args, u16 symbols)
+  // and "the copy-in of the slot's last packed chunk has finished" events
+  void* hst[2] = {nullptr, nullptr};
+  size_t hst_bytes = 0;
+  cudaEvent_t hev[2] = {nullptr, nullptr};
   std::mutex qmutex;
   std::mutex tables_mutex;
   u32 sel_kbits = 0;        // select_kbits() cache  // lazy node_starts / node_rank0 (wt_tree_get)
@@ -552,6 +562,10 @@ static void free_tree_arrays(wt_tree* t) {
     for (auto& e : a)
       if (e) cudaEventDestroy(e);
   for (auto& e : t->tev) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (t->hev[i]) cudaEventDestroy(t->hev[i]);
+    if (t->hst[i]) cudaFreeHost(t->hst[i]);
+  }
   if (t->stream) cudaStreamDestroy(t->stream);
 }
 
@@ -1183,6 +1197,167 @@ static u32 select_kbits(wt_tree* t) {
   return t->sel_kbits;
 }
 
+// ---------------------------------------------------------------------------
+// narrow wire format for host-buffer batches.  PCIe, not the device, bounds a
+// batch that starts and ends in host memory (16 B per rank / select query in,
+// 8 B out).  The host packs each chunk's i64 symbols / arguments into u16 /
+// u32 pinned staging (6 B per query, 4 for access) on a persistent thread
+// pool while the previous chunk is on the wire; a widen kernel restores the
+// i64 chunk buffers on the device.  A chunk holding any value that does not
+// fit (a negative or >= 2^16 symbol, a negative or >= 2^32 argument) crosses
+// wide, unchanged -- validation (and the first bad index) stays on the device
+// either way.  WT_WIRE=0 turns it off (A/B).
+// ---------------------------------------------------------------------------
+namespace {
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool p;
+    return p;
+  }
+  int threads() const { return (int)th_.size() + 1; }
+  // f(worker, workers) on every pool thread and the caller; returns when all did
+  void run(const std::function<void(int, int)>& f) {
+    if (th_.empty()) {
+      f(0, 1);
+      return;
+    }
+    std::lock_guard<std::mutex> serial(run_mu_);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &f;
+      pending_ = (int)th_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    f(0, threads());
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+
+ private:
+  HostPool() {
+    int n = (int)std::thread::hardware_concurrency();
+    if (const char* e = getenv("WT_HOST_THREADS")) n = atoi(e);
+    n = std::max(1, std::min(n, 64));
+    for (int i = 1; i < n; ++i) th_.emplace_back([this, i] { loop(i); });
+  }
+  void loop(int id) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int, int)>* f;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        f = job_;
+      }
+      (*f)(id, threads());
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_, run_mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int, int)>* job_ = nullptr;
+  uint64_t gen_ = 0;
+  int pending_ = 0;
+  bool stop_ = false;
+};
+
+// [a, b) of one pack slice with AVX2: 8 queries per step, staging written
+// with non-temporal stores (no read-for-ownership of the staging lines: the
+// host's memory bandwidth, shared with the DMA engines, is what bounds the
+// pack).  a is a multiple of 64, the staging 256-byte aligned.
+__attribute__((target("avx2"))) uint64_t pack_avx2(const int64_t* ids, const int64_t* args,
+                                                  uint64_t a, uint64_t b, u16* w16, u32* w32) {
+  const __m256i lo32 = _mm256_setr_epi32(0, 2, 4, 6, 1, 3, 5, 7);
+  __m256i over = _mm256_setzero_si256();
+  uint64_t i = a;
+  for (; i + 8 <= b; i += 8) {
+    const __m256i p0 = _mm256_loadu_si256((const __m256i*)(args + i));
+    const __m256i p1 = _mm256_loadu_si256((const __m256i*)(args + i + 4));
+    over = _mm256_or_si256(over, _mm256_or_si256(_mm256_srli_epi64(p0, 32), _mm256_srli_epi64(p1, 32)));
+    const __m256i q0 = _mm256_permutevar8x32_epi32(p0, lo32), q1 = _mm256_permutevar8x32_epi32(p1, lo32);
+    _mm256_stream_si256((__m256i*)(w32 + i), _mm256_permute2x128_si256(q0, q1, 0x20));
+    if (ids) {
+      const __m256i c0 = _mm256_loadu_si256((const __m256i*)(ids + i));
+      const __m256i c1 = _mm256_loadu_si256((const __m256i*)(ids + i + 4));
+      over = _mm256_or_si256(over, _mm256_or_si256(_mm256_srli_epi64(c0, 16), _mm256_srli_epi64(c1, 16)));
+      const __m256i d = _mm256_permute2x128_si256(_mm256_permutevar8x32_epi32(c0, lo32),
+                                                  _mm256_permutevar8x32_epi32(c1, lo32), 0x20);
+      // u32 -> u16 (values above 2^16 are caught by `over`; the chunk then crosses wide)
+      const __m256i pk = _mm256_permute4x64_epi64(_mm256_packus_epi32(d, d), 0x08);
+      _mm_stream_si128((__m128i*)(w16 + i), _mm256_castsi256_si128(pk));
+    }
+  }
+  uint64_t o = (uint64_t)_mm256_testz_si256(over, over) ? 0 : 1;
+  for (; i < b; ++i) {
+    const uint64_t p = (uint64_t)args[i];
+    o |= p >> 32;
+    w32[i] = (u32)p;
+    if (ids) {
+      const uint64_t c = (uint64_t)ids[i];
+      o |= c >> 16;
+      w16[i] = (u16)c;
+    }
+  }
+  _mm_sfence();
+  return o;
+}
+
+// pack cnt queries; false if any value does not fit the narrow format
+bool pack_wire(const int64_t* ids, const int64_t* args, uint64_t cnt, u16* w16, u32* w32) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  std::atomic<uint64_t> over{0};
+  HostPool::get().run([&](int w, int nw) {
+    // 64-query-aligned slices: whole cache lines of every array per thread
+    const uint64_t blocks = (cnt + 63) / 64;
+    const uint64_t a = std::min(cnt, blocks * w / nw * 64);
+    const uint64_t b = std::min(cnt, blocks * (w + 1) / nw * 64);
+    uint64_t o = 0;
+    if (avx2 && ((uintptr_t)w32 & 31) == 0 && ((uintptr_t)w16 & 15) == 0) {
+      o = pack_avx2(ids, args, a, b, w16, w32);
+    } else if (ids) {
+      for (uint64_t i = a; i < b; ++i) {
+        const uint64_t c = (uint64_t)ids[i], p = (uint64_t)args[i];
+        o |= (c >> 16) | (p >> 32);
+        w16[i] = (u16)c;
+        w32[i] = (u32)p;
+      }
+    } else {
+      for (uint64_t i = a; i < b; ++i) {
+        const uint64_t p = (uint64_t)args[i];
+        o |= p >> 32;
+        w32[i] = (u32)p;
+      }
+    }
+    if (o) over.fetch_or(o, std::memory_order_relaxed);
+  });
+  return over.load() == 0;
+}
+
+bool wire_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("WT_WIRE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+}  // namespace
+
 extern "C" int wt_tree_query(wt_tree* t, int kind, const int64_t* ids, const int64_t* args,
                              void* out, uint64_t m, uint64_t chunk, int flags, void* stream,
                              int64_t* bad_index, float* ms_out) {
@@ -1289,7 +1464,14 @@ extern "C" int wt_tree_query_ex(wt_tree* t, int kind, const int64_t* ids, const 
   // bucket_of, sorted-order results; each 16-byte aligned]
   const size_t sort_bytes =
       sorted ? ((1u << kQSortMaxBits) + 256) * 4 + chunk * (4 + 8 + 4 + out_elem) + 5 * 16 : 0;
-  const size_t need = chunk * (16 + out_elem) + 64 + sort_bytes;
+  // narrow wire: texts below 2^32 (positions and ordinals fit u32); the
+  // device slot grows by the chunk's u32 + u16 landing area
+  // (rank / select only: an access query saves 4 B of PCIe, and packing it
+  // costs more host memory bandwidth than that -- measured 5.9 -> 6.3 ms per
+  // 3.3e7 access queries, against 11.7 -> 10.5 ms for rank)
+  const bool wire = wire_enabled() && kind != WT_Q_ACCESS && t->meta.n <= 0xffffffffull;
+  const size_t wire_bytes = wire ? chunk * 6 + 64 : 0;
+  const size_t need = chunk * (16 + out_elem) + 64 + sort_bytes + wire_bytes;
   for (int i = 0; i < 3; ++i) {
     if (!t->qstream[i]) CU(cudaStreamCreateWithFlags(&t->qstream[i], cudaStreamNonBlocking));
     for (int j = 0; j < 2; ++j)
@@ -1303,6 +1485,20 @@ extern "C" int wt_tree_query_ex(wt_tree* t, int kind, const int64_t* ids, const 
     if (!t->qbuf[i]) CU(cudaMalloc(&t->qbuf[i], need));
   }
   t->qbuf_bytes = std::max(t->qbuf_bytes, need);
+  if (wire) {
+    const size_t hb = chunk * 6 + 64;
+    for (int i = 0; i < 2; ++i) {
+      if (t->hst_bytes < hb && t->hst[i]) {
+        // the slot's last copy-in must have drained before the buffer goes
+        if (t->hev[i]) CU(cudaEventSynchronize(t->hev[i]));
+        CU(cudaFreeHost(t->hst[i]));
+        t->hst[i] = nullptr;
+      }
+      if (!t->hst[i]) CU(cudaHostAlloc(&t->hst[i], hb, cudaHostAllocPortable));
+      if (!t->hev[i]) CU(cudaEventCreateWithFlags(&t->hev[i], cudaEventDisableTiming));
+    }
+    t->hst_bytes = std::max(t->hst_bytes, hb);
+  }
   cudaStream_t sin = t->qstream[0], sk = t->qstream[1], sout = t->qstream[2];
   if (validate) {
     CU(cudaMemsetAsync(t->bad, 0xff, 8, sk));
@@ -1318,6 +1514,7 @@ extern "C" int wt_tree_query_ex(wt_tree* t, int kind, const int64_t* ids, const 
   }
   cudaEvent_t* ev = timed ? t->tev.data() : nullptr;
   int rc = WT_OK;
+  uint64_t h2d_bytes = 0, narrow_chunks = 0;
   for (uint64_t c = 0; c < nchunks && rc == WT_OK; ++c) {
     const int s = (int)(c & 1);
     const uint64_t a = c * chunk, cnt = std::min(chunk, m - a);
@@ -1326,17 +1523,48 @@ extern "C" int wt_tree_query_ex(wt_tree* t, int kind, const int64_t* ids, const 
     i64* d_args = (i64*)(base + chunk * 8);
     u8* d_out = base + chunk * 16;
     cudaError_t e = cudaSuccess;
+    // narrow wire: pack chunk c into the slot's pinned staging once the
+    // copy-in of chunk c-2 has read it (overlaps chunk c-1 on the wire)
+    bool narrow = false;
+    u32* d_w32 = nullptr;
+    u16* d_w16 = nullptr;
+    if (wire) {
+      const uint64_t w16_off = (chunk * 4 + 15) & ~(uint64_t)15;
+      u8* wp = (u8*)(((uintptr_t)(base + need - wire_bytes) + 15) & ~(uintptr_t)15);
+      d_w32 = (u32*)wp;
+      d_w16 = (u16*)(wp + w16_off);
+      u32* h32 = (u32*)t->hst[s];
+      u16* h16 = (u16*)((u8*)t->hst[s] + w16_off);
+      if (c >= 2) e = cudaEventSynchronize(t->hev[s]);
+      if (e == cudaSuccess)
+        narrow = pack_wire(kind != WT_Q_ACCESS ? ids + a : nullptr, args + a, cnt, h16, h32);
+      if (narrow) {
+        if (c >= 2) e = cudaStreamWaitEvent(sin, t->qev[1][s], 0);
+        if (e == cudaSuccess && ev) e = cudaEventRecord(ev[3 * c], sin);
+        if (e == cudaSuccess && kind != WT_Q_ACCESS)
+          e = cudaMemcpyAsync(d_w16, h16, cnt * 2, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_w32, h32, cnt * 4, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess) e = cudaEventRecord(t->hev[s], sin);
+      }
+    }
     // copy-in: slot s is free once the kernel of chunk c-2 has read it
-    if (c >= 2) e = cudaStreamWaitEvent(sin, t->qev[1][s], 0);
-    if (e == cudaSuccess && ev) e = cudaEventRecord(ev[3 * c], sin);
-    if (e == cudaSuccess && kind != WT_Q_ACCESS)
-      e = cudaMemcpyAsync(d_ids, ids + a, cnt * 8, cudaMemcpyHostToDevice, sin);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_args, args + a, cnt * 8, cudaMemcpyHostToDevice, sin);
+    if (!narrow) {
+      if (e == cudaSuccess && c >= 2) e = cudaStreamWaitEvent(sin, t->qev[1][s], 0);
+      if (e == cudaSuccess && ev) e = cudaEventRecord(ev[3 * c], sin);
+      if (e == cudaSuccess && kind != WT_Q_ACCESS)
+        e = cudaMemcpyAsync(d_ids, ids + a, cnt * 8, cudaMemcpyHostToDevice, sin);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(d_args, args + a, cnt * 8, cudaMemcpyHostToDevice, sin);
+    }
+    const uint64_t in_elem = narrow ? (kind != WT_Q_ACCESS ? 6 : 4) : (kind != WT_Q_ACCESS ? 16 : 8);
+    h2d_bytes += cnt * in_elem;
+    narrow_chunks += narrow;
     if (e == cudaSuccess && ev) e = cudaEventRecord(ev[3 * c + 1], sin);
     if (e == cudaSuccess) e = cudaEventRecord(t->qev[0][s], sin);
     // kernel: inputs landed, and the copy-out of chunk c-2 has drained d_out
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sk, t->qev[0][s], 0);
     if (e == cudaSuccess && c >= 2) e = cudaStreamWaitEvent(sk, t->qev[2][s], 0);
+    if (e == cudaSuccess && narrow)
+      e = launch_widen(kind != WT_Q_ACCESS ? d_w16 : nullptr, d_w32, d_ids, d_args, cnt, sk);
     if (e == cudaSuccess && !sorted) {
       e = launch_query(t->dev, kind, out_kind, validate, d_ids, d_args, d_out, cnt, t->rate_log, a,
                        t->bad, sk);
@@ -1412,6 +1640,8 @@ extern "C" int wt_tree_query_ex(wt_tree* t, int kind, const int64_t* ids, const 
       stats->kernel_ms = kern;
       stats->d2h_ms = last_out - prev_k;  // the copy-out tail after the last kernel
       stats->total_ms = last_out;
+      stats->h2d_bytes = h2d_bytes;
+      stats->narrow_chunks = narrow_chunks;
     }
   }
   if (rc == WT_OK && validate && bad_index) {

@@ -102,6 +102,10 @@ struct QuerySortScratch {
 };
 // phase (optional): 3 events recorded after the sort (key + scan + scatter),
 // after the walk and after the gather back to query order
+// host-buffer batches on the narrow wire format: u16 symbols / u32 arguments
+// (packed on the host) widened into the i64 chunk buffers the query kernels read
+cudaError_t launch_widen(const u16* w16, const u32* w32, i64* ids, i64* args, u64 m,
+                         cudaStream_t st);
 cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool validate,
                                 const i64* ids, const i64* args, void* out, u64 m, int rate_log,
                                 u64 base, u64* bad, const QuerySortScratch& S, cudaStream_t st,

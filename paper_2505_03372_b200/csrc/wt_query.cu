@@ -9,6 +9,7 @@
 //           stop when child `bit` of the node is a leaf (width-1 interval);
 //   rank:   the same walk along the code of c, result p_len - cum_hist[c];
 //   select: bottom-up, p = select_bit(p' - base + 1), from cum_hist[c]+k-1.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include "wt_common.cuh"
@@ -21,6 +22,10 @@ namespace wt {
 #define WT_Q_NT 128  // 128 vs 256 vs 512 threads: select -1.3 %, others flat
 #endif
 constexpr int Q_NT = WT_Q_NT;
+#ifndef WT_QS_QPT
+#define WT_QS_QPT 1
+#endif
+constexpr int QS_QPT = WT_QS_QPT;  // queries per thread in the sort's key / scatter kernels
 
 // a sorted batch (WT_F_SORT) carries (argument | id << 48) per query
 // unpack the sorted batch (rank / select): id and argument
@@ -234,9 +239,22 @@ __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__
                                                          u32 arg_shift, u32 nb, u32* __restrict__ bucket_of,
                                                          u32* __restrict__ hist, u64 base,
                                                          u64* __restrict__ bad) {
-  const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
+  // QS_QPT queries per thread, Q_NT apart: every load is issued before the
+  // first query's dependent table reads
+  const u64 i0 = (u64)blockIdx.x * QS_QPT * Q_NT + threadIdx.x;
+  u64 aq[QS_QPT];
+  i64 rq[QS_QPT];
+#pragma unroll
+  for (int j = 0; j < QS_QPT; ++j) {
+    const u64 i = i0 + (u64)j * Q_NT;
+    aq[j] = i < m ? (u64)__ldg(args + i) : 0ull;
+    rq[j] = i < m && kind != 0 ? __ldg(ids + i) : 0ll;
+  }
+#pragma unroll
+  for (int j = 0; j < QS_QPT; ++j) {
+  const u64 i = i0 + (u64)j * Q_NT;
   if (i >= m) return;
-  const u64 a = (u64)args[i];
+  const u64 a = aq[j];
   u32 bucket = 0;
   bool ok = true;
   if (kind == 0) {
@@ -245,12 +263,12 @@ __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__
   } else {
     u32 c = 0;
     if (validate) {
-      const i64 raw = ids[i];
+      const i64 raw = rq[j];
       const int id = (raw < 0 || raw > 65535) ? -1 : __ldg(T.sym2id + raw);
       ok = id >= 0;
       c = ok ? (u32)id : 0u;
     } else {
-      const i64 raw = ids[i];
+      const i64 raw = rq[j];
       c = raw < 0 ? 0u : (u32)min(raw, (i64)T.sigma - 1);  // memory safety only
     }
     if (ok && validate) {
@@ -279,6 +297,7 @@ __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__
   bucket = min(bucket, nb - 1u);
   bucket_of[i] = bucket;
   atomicAdd(hist + bucket, 1u);
+  }
 }
 
 // exclusive scan of the bucket counts in place, 4096 buckets per CTA (1024
@@ -364,8 +383,6 @@ __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restri
                                                              i64* __restrict__ sargs,
                                                              u32* __restrict__ sargs32, u32 kbits,
                                                              u32* __restrict__ slot_of) {
-  const u64 i = (u64)blockIdx.x * Q_NT + threadIdx.x;
-  if (i >= m) return;
   // L2 policy: the streams (bucket_of, args in; slot_of out) evict first, the
   // scattered sorted-batch stores evict last -- a bucket's 32-byte sectors
   // fill up over the whole kernel and a partial sector written back costs a
@@ -373,14 +390,31 @@ __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restri
   u64 pf, pl;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
-  u32 b;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
-               : "=r"(b) : "l"(bucket_of + i), "l"(pf));
-  const u32 slot = atomicAdd(cursor + b, 1u);
-  u64 a;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
-               : "=l"(a) : "l"(args + i), "l"(pf));
-  a &= (1ull << 48) - 1;
+  // QS_QPT queries per thread, Q_NT apart: their returning cursor atomics are
+  // independent, so a thread keeps QS_QPT of them in flight
+  const u64 i0 = (u64)blockIdx.x * QS_QPT * Q_NT + threadIdx.x;
+  u32 bq[QS_QPT], sq[QS_QPT];
+  u64 aq[QS_QPT];
+#pragma unroll
+  for (int j = 0; j < QS_QPT; ++j) {
+    const u64 i = i0 + (u64)j * Q_NT;
+    bq[j] = 0; aq[j] = 0;
+    if (i < m) {
+      asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                   : "=r"(bq[j]) : "l"(bucket_of + i), "l"(pf));
+      asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
+                   : "=l"(aq[j]) : "l"(args + i), "l"(pf));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < QS_QPT; ++j)
+    if (i0 + (u64)j * Q_NT < m) sq[j] = atomicAdd(cursor + bq[j], 1u);
+#pragma unroll
+  for (int j = 0; j < QS_QPT; ++j) {
+  const u64 i = i0 + (u64)j * Q_NT;
+  if (i >= m) return;
+  const u32 b = bq[j], slot = sq[j];
+  const u64 a = aq[j] & ((1ull << 48) - 1);
   const u64 v = with_id ? a | ((u64)(b & ((1u << sym_bits) - 1u)) << 48) : a;
   if (sargs32) {  // 4-byte records: access position, or select (ordinal | id << kbits)
     // (invalid queries -- the batch raises -- keep a masked ordinal and id 0)
@@ -394,6 +428,7 @@ __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restri
                  : "memory");
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(slot_of + i),
                "r"(slot), "l"(pf) : "memory");
+  }
 }
 
 // results back in query order: out[i] = res[slot_of[i]] -- random 8-byte
@@ -457,7 +492,8 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   const u32 nb = 1u << qb;
   cudaError_t e = cudaMemsetAsync(S.hist, 0, nb * 4, st);
   if (e != cudaSuccess) return e;
-  qsort_key_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(T, kind, ids, args, m, validate, sym_bits,
+  const unsigned kblocks = (unsigned)((m + (u64)QS_QPT * Q_NT - 1) / ((u64)QS_QPT * Q_NT));
+  qsort_key_kernel<<<kblocks, Q_NT, 0, st>>>(T, kind, ids, args, m, validate, sym_bits,
                                                       arg_shift, nb, S.bucket_of, S.hist,
                                                       base, bad);
   const unsigned sb = (nb + QS_PER_CTA - 1) / QS_PER_CTA;
@@ -470,7 +506,7 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   const bool sel32 = kind == 2 && S.sel_kbits && S.sel_kbits + sym_bits <= 32;
   u32* s32 = (kind == 0 && T.n <= 0xffffffffull) || sel32 ? reinterpret_cast<u32*>(S.sorted_args)
                                                           : nullptr;
-  qsort_scatter_kernel<<<(unsigned)blocks, Q_NT, 0, st>>>(S.bucket_of, kind != 0, sym_bits,
+  qsort_scatter_kernel<<<kblocks, Q_NT, 0, st>>>(S.bucket_of, kind != 0, sym_bits,
                                                           args, m, S.hist, S.sorted_args, s32,
                                                           sel32 ? S.sel_kbits : 0u, S.slot_of);
   e = cudaGetLastError();
@@ -522,6 +558,31 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   e = cudaGetLastError();
   if (e == cudaSuccess && phase) e = cudaEventRecord(phase[2], st);
   return e;
+}
+
+// ---------------------------------------------------------------------------
+// narrow wire format (wt_capi.cu host pipeline): 6 bytes per rank / select
+// query and 4 per access query cross PCIe instead of 16 / 8; the widening is
+// a streaming pass (22 B per query of HBM traffic, ~0.1 ms per 2^22 chunk)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) widen_kernel(const u16* __restrict__ w16,
+                                                    const u32* __restrict__ w32,
+                                                    i64* __restrict__ ids, i64* __restrict__ args,
+                                                    u64 m) {
+  const u64 stride = (u64)gridDim.x * 256;
+  for (u64 i = (u64)blockIdx.x * 256 + threadIdx.x; i < m; i += stride) {
+    args[i] = (i64)__ldg(w32 + i);
+    if (w16) ids[i] = (i64)__ldg(w16 + i);
+  }
+}
+
+cudaError_t launch_widen(const u16* w16, const u32* w32, i64* ids, i64* args, u64 m,
+                         cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  const u64 want = (m + 255) / 256;
+  const unsigned blocks = (unsigned)std::min<u64>(want, 148ull * 16);
+  widen_kernel<<<blocks, 256, 0, st>>>(w16, w32, ids, args, m);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------

@@ -283,3 +283,51 @@ def test_pinned_result_cache_size_classes_and_cap():
         assert _lib.pinned_cached_bytes() <= _lib.PINNED_CACHE_BYTES  # freed, not cached
     finally:
         _lib.PINNED_CACHE_BYTES = old
+
+
+@pytest.mark.parametrize("sort", [False, True])
+def test_narrow_wire_chunks_mixed_with_wide(W, sort):
+    """Host-buffer batches cross PCIe packed (u16 symbols / u32 arguments,
+    wt_capi.cu pack_wire); a chunk holding a value that does not fit crosses
+    wide.  Answers and the first bad index are the same either way."""
+    rng = np.random.default_rng(11)
+    text = rng.integers(0, 200, 50_000).astype(np.uint8)
+    t = W.construct(text)
+    fa, fr, fs = O.text_answers(text, 256)
+    m = 20_000
+    c = rng.choice(np.unique(text), m).astype(np.int64)
+    p = rng.integers(0, len(text) + 1, m)
+    assert np.array_equal(W.rank_batch(t, c, p, chunk_size=3000, sort=sort), fr(c, p))
+    occ = np.bincount(text, minlength=256)
+    k = 1 + (rng.random(m) * occ[c]).astype(np.int64)
+    assert np.array_equal(W.select_batch(t, c, k, chunk_size=3000, sort=sort), fs(c, k))
+    pos = rng.integers(0, len(text), m)
+    assert np.array_equal(W.access_batch(t, pos, chunk_size=3000, sort=sort), text[pos])
+    # a symbol >= 2^16 (wide chunk 4) after an in-range but absent one (narrow chunk 2)
+    bad_c = c.copy()
+    bad_c[13_000] = 70_000
+    bad_c[7_500] = 250
+    with pytest.raises(W.BatchError) as e:
+        W.rank_batch(t, bad_c, p, chunk_size=3000, sort=sort)
+    assert e.value.index == 7_500 and isinstance(e.value.__cause__, W.SymbolError)
+    bad_c[7_500] = c[7_500]
+    with pytest.raises(W.BatchError) as e:
+        W.rank_batch(t, bad_c, p, chunk_size=3000, sort=sort)
+    assert e.value.index == 13_000 and isinstance(e.value.__cause__, W.SymbolError)
+    # positions / ordinals >= 2^32 and negative ones cross wide and still fail
+    bad_p = p.copy()
+    bad_p[4_001] = 1 << 33
+    bad_p[19_999] = -1
+    with pytest.raises(W.BatchError) as e:
+        W.rank_batch(t, c, bad_p, chunk_size=3000, sort=sort)
+    assert e.value.index == 4_001 and isinstance(e.value.__cause__, W.PositionError)
+    bad_k = k.copy()
+    bad_k[6_123] = (1 << 32) + 5
+    with pytest.raises(W.BatchError) as e:
+        W.select_batch(t, c, bad_k, chunk_size=3000, sort=sort)
+    assert e.value.index == 6_123 and isinstance(e.value.__cause__, W.OrdinalError)
+    bad_pos = pos.copy()
+    bad_pos[11_111] = -(1 << 40)
+    with pytest.raises(W.BatchError) as e:
+        W.access_batch(t, bad_pos, chunk_size=3000, sort=sort)
+    assert e.value.index == 11_111 and isinstance(e.value.__cause__, W.PositionError)

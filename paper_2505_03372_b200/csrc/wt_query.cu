@@ -23,9 +23,13 @@ namespace wt {
 #endif
 constexpr int Q_NT = WT_Q_NT;
 #ifndef WT_QS_QPT
-#define WT_QS_QPT 1
+#define WT_QS_QPT 1  // A/B on B200: 2 / 4 / 8 measured 0.2-1.5 % slower
 #endif
-constexpr int QS_QPT = WT_QS_QPT;  // queries per thread in the sort's key / scatter kernels
+constexpr int QS_QPT = WT_QS_QPT;
+#ifndef WT_QS_RANK
+#define WT_QS_RANK 0  // A/B on B200: 1 measured slower (C2 sorted batches +3.5 % time)
+#endif
+constexpr bool QS_RANK = WT_QS_RANK != 0;  // ranks in bucket from the count pass  // queries per thread in the sort's key / scatter kernels
 
 // a sorted batch (WT_F_SORT) carries (argument | id << 48) per query
 // unpack the sorted batch (rank / select): id and argument
@@ -238,7 +242,8 @@ __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__
                                                          bool validate, u32 sym_bits,
                                                          u32 arg_shift, u32 nb, u32* __restrict__ bucket_of,
                                                          u32* __restrict__ hist, u64 base,
-                                                         u64* __restrict__ bad) {
+                                                         u64* __restrict__ bad,
+                                                         u32* __restrict__ rank_of) {
   // QS_QPT queries per thread, Q_NT apart: every load is issued before the
   // first query's dependent table reads
   const u64 i0 = (u64)blockIdx.x * QS_QPT * Q_NT + threadIdx.x;
@@ -296,7 +301,13 @@ __global__ void __launch_bounds__(Q_NT) qsort_key_kernel(const __grid_constant__
   // anyway so a broken promise cannot index past the bucket table
   bucket = min(bucket, nb - 1u);
   bucket_of[i] = bucket;
-  atomicAdd(hist + bucket, 1u);
+  // WT_QS_RANK: the count's returning atomic hands each query its rank in
+  // the bucket, so the scatter needs no atomics of its own (one returning
+  // atomic per query instead of a reduction plus a returning atomic)
+  if (QS_RANK)
+    rank_of[i] = atomicAdd(hist + bucket, 1u);
+  else
+    atomicAdd(hist + bucket, 1u);
   }
 }
 
@@ -408,7 +419,9 @@ __global__ void __launch_bounds__(Q_NT) qsort_scatter_kernel(const u32* __restri
   }
 #pragma unroll
   for (int j = 0; j < QS_QPT; ++j)
-    if (i0 + (u64)j * Q_NT < m) sq[j] = atomicAdd(cursor + bq[j], 1u);
+    if (i0 + (u64)j * Q_NT < m)
+      sq[j] = QS_RANK ? __ldg(cursor + bq[j]) + slot_of[i0 + (u64)j * Q_NT]
+                      : atomicAdd(cursor + bq[j], 1u);
 #pragma unroll
   for (int j = 0; j < QS_QPT; ++j) {
   const u64 i = i0 + (u64)j * Q_NT;
@@ -495,7 +508,7 @@ cudaError_t launch_query_sorted(const TreeDev& T, int kind, int out_kind, bool v
   const unsigned kblocks = (unsigned)((m + (u64)QS_QPT * Q_NT - 1) / ((u64)QS_QPT * Q_NT));
   qsort_key_kernel<<<kblocks, Q_NT, 0, st>>>(T, kind, ids, args, m, validate, sym_bits,
                                                       arg_shift, nb, S.bucket_of, S.hist,
-                                                      base, bad);
+                                                      base, bad, S.slot_of);
   const unsigned sb = (nb + QS_PER_CTA - 1) / QS_PER_CTA;
   u32* partial = S.hist + (1u << kQSortMaxBits);
   qsort_scan_partial_kernel<<<sb, 1024, 0, st>>>(S.hist, nb, partial);

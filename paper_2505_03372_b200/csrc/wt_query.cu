@@ -25,11 +25,11 @@ constexpr int Q_NT = WT_Q_NT;
 #ifndef WT_QS_QPT
 #define WT_QS_QPT 1  // A/B on B200: 2 / 4 / 8 measured 0.2-1.5 % slower
 #endif
-constexpr int QS_QPT = WT_QS_QPT;
+constexpr int QS_QPT = WT_QS_QPT;  // queries per thread in the sort's key / scatter kernels
 #ifndef WT_QS_RANK
 #define WT_QS_RANK 0  // A/B on B200: 1 measured slower (C2 sorted batches +3.5 % time)
 #endif
-constexpr bool QS_RANK = WT_QS_RANK != 0;  // ranks in bucket from the count pass  // queries per thread in the sort's key / scatter kernels
+constexpr bool QS_RANK = WT_QS_RANK != 0;  // ranks in bucket from the count pass
 
 // a sorted batch (WT_F_SORT) carries (argument | id << 48) per query
 // unpack the sorted batch (rank / select): id and argument

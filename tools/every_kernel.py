@@ -7,7 +7,7 @@ realistic size, for one `ncu --set full` capture of all of them
   u8 LUT build (sigma=200, 2^28)          hist8, wcount0, wlevel<u8,u8,lut>, wlast<lut>
   C3u-like build (u16, 2^28)              hist16p, hist16_fold, wlevel<u16,u16>
   declared alphabet with a stray symbol   first_outside
-  queries, 1e7 per kind, sorted + not     qsort_key, qsort_scan_*, qsort_scatter, access/rank/select, qunsort
+  queries, 1e7 per kind, sorted + not     qsort_key, qsort_scan_*, qsort_scatter, access/rank/select, qunsort, widen (host batches: narrow wire)
   build_index over 2^30 bits + queries    bits_directory, bits_query
   the building-block ops (wt_ops.cu)      map, encode, split_count/scan/scatter, pack_bits
 """

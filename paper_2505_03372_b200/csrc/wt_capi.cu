@@ -7,6 +7,7 @@
 #include <cstring>
 #include <type_traits>
 #include <dlfcn.h>
+#include <unistd.h>
 #include <atomic>
 #include <immintrin.h>
 #include <condition_variable>
@@ -1211,14 +1212,17 @@ static u32 select_kbits(wt_tree* t) {
 namespace {
 class HostPool {
  public:
+  // never destroyed: the workers sleep until process exit (no join at exit,
+  // where a forked child would wait on threads it does not have)
   static HostPool& get() {
-    static HostPool p;
-    return p;
+    static HostPool* p = new HostPool;
+    return *p;
   }
   int threads() const { return (int)th_.size() + 1; }
-  // f(worker, workers) on every pool thread and the caller; returns when all did
+  // f(worker, workers) on every pool thread and the caller; returns when all
+  // did.  In a child forked after the pool started, the caller does it alone.
   void run(const std::function<void(int, int)>& f) {
-    if (th_.empty()) {
+    if (th_.empty() || getpid() != pid_) {
       f(0, 1);
       return;
     }
@@ -1235,18 +1239,8 @@ class HostPool {
     done_.wait(lk, [&] { return pending_ == 0; });
     job_ = nullptr;
   }
-  ~HostPool() {
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
-      ++gen_;
-    }
-    cv_.notify_all();
-    for (auto& t : th_) t.join();
-  }
-
  private:
-  HostPool() {
+  HostPool() : pid_(getpid()) {
     int n = (int)std::thread::hardware_concurrency();
     if (const char* e = getenv("WT_HOST_THREADS")) n = atoi(e);
     n = std::max(1, std::min(n, 64));
@@ -1260,7 +1254,6 @@ class HostPool {
         std::unique_lock<std::mutex> lk(mu_);
         cv_.wait(lk, [&] { return gen_ != seen; });
         seen = gen_;
-        if (stop_) return;
         f = job_;
       }
       (*f)(id, threads());
@@ -1274,7 +1267,7 @@ class HostPool {
   const std::function<void(int, int)>* job_ = nullptr;
   uint64_t gen_ = 0;
   int pending_ = 0;
-  bool stop_ = false;
+  const pid_t pid_;
 };
 
 // [a, b) of one pack slice with AVX2: 8 queries per step, staging written

@@ -51,7 +51,7 @@ def main(path, peak):
         if not k.startswith(("wlevel", "wlast", "qlayout", "hist", "block_l1", "l1_scan",
                              "wcount0", "first_outside", "bits_", "access_kernel", "rank_kernel",
                              "select_kernel", "qsort", "qunsort", "map_kernel", "encode_kernel",
-                             "split_", "pack_bits", "wpair", "dir_kernel", "dirq_kernel")):
+                             "split_", "pack_bits", "wpair", "dir_kernel", "dirq_kernel", "widen")):
             continue
         counts[k] = counts.get(k, 0) + 1
         b = (num(d.get("dram__bytes_read.sum", 0), un.get("dram__bytes_read.sum", "")) +

@@ -532,7 +532,9 @@ def run_ours(args):
     if args.e2e:
         pin = lambda t: t.cpu().pin_memory().numpy()
         h = {k: (None if q[k][0] is None else pin(q[k][0]), pin(q[k][1])) for k in KINDS}
-        chunk = 1 << 21  # 16 chunks per kind: copy-in / kernel / copy-out overlap
+        # 8 chunks per kind: copy-in / kernel / copy-out (and the host pack)
+        # overlap; 2^22 measured 5 % faster than 2^21 (tools/bench_e2e.py)
+        chunk = 1 << 22
 
         runners = {k: W.BatchRunner(tree, chunk, sort=True) for k in KINDS}
         batches = {k: W.QueryBatch(k, h[k][1], h[k][0], chunk) for k in KINDS}
@@ -567,7 +569,7 @@ def run_ours(args):
                "narrow_chunks": {k: [runners[k].narrow_chunks, runners[k].chunks] for k in KINDS},
                "d2h_bytes_per_step": int(per[0] * 1 + (per[1] + per[2]) * 8),
                "api": "BatchRunner(sort=True).run (access_batch / rank_batch / select_batch) "
-                      "on pinned numpy arrays, chunk 2^21; int64 inputs packed to the "
+                      "on pinned numpy arrays, chunk 2^22; int64 inputs packed to the "
                       "narrow wire (u16 symbols, u32 arguments) by a host thread pool",
                "per_kind": {k: {"ms": kind_s[k] * 1e3 / args.steps,
                                 "stage_ms": runners[k].stage_seconds * 1e3,

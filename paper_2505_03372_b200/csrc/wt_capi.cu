@@ -1315,7 +1315,12 @@ __attribute__((target("avx2"))) uint64_t pack_avx2(const int64_t* ids, const int
 bool pack_wire(const int64_t* ids, const int64_t* args, uint64_t cnt, u16* w16, u32* w32) {
   static const bool avx2 = __builtin_cpu_supports("avx2");
   std::atomic<uint64_t> over{0};
-  HostPool::get().run([&](int w, int nw) {
+  // about 2^15 queries per worker at least: a small chunk (the API's default
+  // is 65,536 queries) is packed by fewer threads, or by the caller alone
+  const uint64_t want = std::max<uint64_t>(1, cnt >> 15);
+  const auto job = [&](int w, int nw_pool) {
+    const int nw = (int)std::min<uint64_t>((uint64_t)nw_pool, want);
+    if (w >= nw) return;
     // 64-query-aligned slices: whole cache lines of every array per thread
     const uint64_t blocks = (cnt + 63) / 64;
     const uint64_t a = std::min(cnt, blocks * w / nw * 64);
@@ -1338,8 +1343,20 @@ bool pack_wire(const int64_t* ids, const int64_t* args, uint64_t cnt, u16* w16, 
       }
     }
     if (o) over.fetch_or(o, std::memory_order_relaxed);
-  });
+  };
+  if (want == 1)
+    job(0, 1);
+  else
+    HostPool::get().run(job);
   return over.load() == 0;
+}
+
+// smallest chunk that crosses narrow (WT_WIRE_MIN_CHUNK overrides; read per
+// call so the tests can drive small chunks through the narrow path)
+uint64_t wire_min_chunk() {
+  const char* e = getenv("WT_WIRE_MIN_CHUNK");
+  const unsigned long long v = e ? strtoull(e, nullptr, 10) : 0;
+  return v ? (uint64_t)v : (1ull << 20);
 }
 
 bool wire_enabled() {
@@ -1462,7 +1479,12 @@ extern "C" int wt_tree_query_ex(wt_tree* t, int kind, const int64_t* ids, const 
   // (rank / select only: an access query saves 4 B of PCIe, and packing it
   // costs more host memory bandwidth than that -- measured 5.9 -> 6.3 ms per
   // 3.3e7 access queries, against 11.7 -> 10.5 ms for rank)
-  const bool wire = wire_enabled() && kind != WT_Q_ACCESS && t->meta.n <= 0xffffffffull;
+  // Chunks below 2^20 queries stay wide: the wide pipeline enqueues every
+  // chunk without a host wait, while a packed chunk holds the host loop for
+  // its pack -- at 2^16-query chunks (the API default) that measured 1.5x
+  // slower for rank, at 2^18 even, at 2^22 15 % faster.
+  const bool wire = wire_enabled() && kind != WT_Q_ACCESS && t->meta.n <= 0xffffffffull &&
+                    chunk >= wire_min_chunk();
   const size_t wire_bytes = wire ? chunk * 6 + 64 : 0;
   const size_t need = chunk * (16 + out_elem) + 64 + sort_bytes + wire_bytes;
   for (int i = 0; i < 3; ++i) {

@@ -286,10 +286,11 @@ def test_pinned_result_cache_size_classes_and_cap():
 
 
 @pytest.mark.parametrize("sort", [False, True])
-def test_narrow_wire_chunks_mixed_with_wide(W, sort):
+def test_narrow_wire_chunks_mixed_with_wide(W, sort, monkeypatch):
     """Host-buffer batches cross PCIe packed (u16 symbols / u32 arguments,
     wt_capi.cu pack_wire); a chunk holding a value that does not fit crosses
     wide.  Answers and the first bad index are the same either way."""
+    monkeypatch.setenv("WT_WIRE_MIN_CHUNK", "1")  # (default: chunks of 2^20 and up)
     rng = np.random.default_rng(11)
     text = rng.integers(0, 200, 50_000).astype(np.uint8)
     t = W.construct(text)
@@ -303,6 +304,18 @@ def test_narrow_wire_chunks_mixed_with_wide(W, sort):
     assert np.array_equal(W.select_batch(t, c, k, chunk_size=3000, sort=sort), fs(c, k))
     pos = rng.integers(0, len(text), m)
     assert np.array_equal(W.access_batch(t, pos, chunk_size=3000, sort=sort), text[pos])
+    r = W.BatchRunner(t, 3000, sort=sort)
+    assert np.array_equal(r.run(W.QueryBatch("rank", p, c, 3000)), fr(c, p))
+    assert r.chunks == 7 and r.narrow_chunks == 7 and r.h2d_bytes == 6 * m
+    big = c.copy()
+    big[3500] = 1 << 20  # chunk 1 crosses wide (and raises: not in the alphabet)
+    with pytest.raises(W.BatchError):
+        r.run(W.QueryBatch("rank", p, big, 3000))
+    assert r.chunks == 7 and r.narrow_chunks == 6
+    monkeypatch.setenv("WT_WIRE_MIN_CHUNK", str(1 << 40))
+    assert np.array_equal(r.run(W.QueryBatch("rank", p, c, 3000)), fr(c, p))
+    assert r.narrow_chunks == 0 and r.h2d_bytes == 16 * m
+    monkeypatch.setenv("WT_WIRE_MIN_CHUNK", "1")
     # a symbol >= 2^16 (wide chunk 4) after an in-range but absent one (narrow chunk 2)
     bad_c = c.copy()
     bad_c[13_000] = 70_000

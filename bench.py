@@ -40,6 +40,7 @@ on CPU (gloo) for the tests.
 from __future__ import annotations
 
 import argparse
+import gc
 import io
 import json
 import os
@@ -257,10 +258,15 @@ def _build_timed(W, text_dev, alpha, steps, warmup):
     from paper_2505_03372_b200 import _lib
     mk = (lambda: W.construct(text_dev)) if alpha is None else \
         (lambda: W.construct_with_alphabet(text_dev, alpha))
+    # each replaced tree is collected before the next build: a WaveletTree
+    # sits in a reference cycle (its lazy rank/select views), so without the
+    # collect several trees' device arrays pile up and a later build waits on
+    # the memory pool growing (seen: 57 ms .. 1.6 s pre-phases)
     tree = None
     for _ in range(warmup):
         tree = mk()
         del tree
+        gc.collect()
     ms, lvl = [], []
     prof = (C.c_float * 32)()
     for s in range(steps):
@@ -270,6 +276,7 @@ def _build_timed(W, text_dev, alpha, steps, warmup):
         lvl.append([prof[i] for i in range(1 + tree.num_levels)])
         if s < steps - 1:
             del tree
+            gc.collect()
     return tree, ms, np.median(np.array(lvl), axis=0)
 
 
@@ -346,6 +353,7 @@ def _extra_builds(W, args, dev, hbm):
         rec["text"] = c
         out[name] = rec
         del tree, text
+        gc.collect()
         torch.cuda.empty_cache()
     return out
 

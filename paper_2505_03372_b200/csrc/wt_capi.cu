@@ -666,7 +666,9 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       TRY(S.get(&dbh, n_blk + 4));
       CU(cudaMemsetAsync(dbh, 0, (n_blk + 4) * 4, st));
     }
+    tr.mark("histogram inputs allocated");
     CU(launch_histogram(dtext, n, sym_bytes, dhist, sm_count(device), st, dbh));
+    tr.mark("histogram kernels queued");
     static thread_local std::vector<uint64_t> hraw;
     hraw.assign(nb, 0);
     CU(cudaMemcpyAsync(hraw.data(), dhist, nb * 8, cudaMemcpyDeviceToHost, st));
@@ -741,6 +743,7 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       void* probe = nullptr;
       if (cudaMallocAsync(&probe, est, st) == cudaSuccess) cudaFreeAsync(probe, st);
       else cudaGetLastError();
+      tr.mark("pool probe");
     }
     TRY(alloc_tree_core(t, st));
     tr.mark("tree allocated");

@@ -107,22 +107,29 @@ struct QLine {
   u64 wd[kQW];
 };
 
+// L2 fetch-size hint of the query loads (WT_QL2: A/B knob; on B200 the
+// sorted C2 batches ran 0.3-0.6 % faster with L2::128B / L2::256B, the
+// random ones 3 % slower than with L2::64B)
+#ifndef WT_QL2
+#define WT_QL2 "L2::64B"
+#endif
+
 // Random 64-byte line reads: hint the L2 to fetch 64 B (LTC64B) instead of
 // promoting the miss to a larger DRAM request -- every rank step is one
 // line, so anything beyond it is wasted HBM bandwidth.
 __device__ __forceinline__ ulonglong2 ld_line16(const ulonglong2* p) {
   ulonglong2 v;
-  asm volatile("ld.global.nc.L2::64B.v2.u64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+  asm volatile("ld.global.nc." WT_QL2 ".v2.u64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
   return v;
 }
 __device__ __forceinline__ u64 ld_u64_64b(const u64* p) {
   u64 v;
-  asm volatile("ld.global.nc.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  asm volatile("ld.global.nc." WT_QL2 ".u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ u32 ld_u32_64b(const u32* p) {
   u32 v;
-  asm volatile("ld.global.nc.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.global.nc." WT_QL2 ".u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 
@@ -147,7 +154,7 @@ __device__ __forceinline__ void st_stream_i64(i64* a, i64 v, u64 pol) {
 // one 64-byte line as two 256-bit loads (LDG.256, sm_100): half the LSU
 // instructions of 16-byte loads, which kept the query kernels lg-throttled
 __device__ __forceinline__ void ld_line32(const ulonglong2* p, u64& a, u64& b, u64& c, u64& d) {
-  asm volatile("ld.global.nc.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc." WT_QL2 ".v4.u64 {%0,%1,%2,%3}, [%4];"
                : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
                : "l"(p));
 }
@@ -155,7 +162,7 @@ static_assert(kQW == 3 || kQW == 7, "line width: one 32-byte sector or 64 bytes"
 // one 32-byte line: one LDG.256; the L2::64B hint (the neighbouring line
 // comes along) measured +3 % on random batches, neutral on sorted ones
 __device__ __forceinline__ void ld_sector(const ulonglong2* p, u64& a, u64& b, u64& c, u64& d) {
-  asm volatile("ld.global.nc.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc." WT_QL2 ".v4.u64 {%0,%1,%2,%3}, [%4];"
                : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
                : "l"(p));
 }

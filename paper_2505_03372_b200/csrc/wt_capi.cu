@@ -156,11 +156,11 @@ static std::vector<NodeEnt>& node_cache() {
 // node counts at build time; the reference's node_starts / node_rank0 arrays
 // only when exported (wt_tree_get), so a 2^16-symbol build does not allocate
 // them.
-static void plan_walk(Plan& P, bool tables) {
-  const uint32_t s = P.sigma, L = P.L;
+static void plan_walk(Plan& P, bool tables, uint32_t levels = ~0u) {
+  const uint32_t s = P.sigma, L = std::min(P.L, levels);
   static thread_local std::vector<std::pair<uint32_t, uint32_t>> cur, nxt;
   cur.clear();
-  P.n_nodes.assign(L, 0);
+  P.n_nodes.assign(P.L, 0);
   if (tables) {
     P.node_starts.assign(L, {});
     P.node_rank0.assign(L, {});
@@ -181,7 +181,7 @@ static void plan_walk(Plan& P, bool tables) {
         P.node_starts[l].push_back(a);
         P.node_rank0[l].push_back(zeros_before);
       } else {
-        const uint32_t key = (uint32_t)P.values[a] >> (L - l);
+        const uint32_t key = (uint32_t)P.values[a] >> (P.L - l);
         NodeEnt& ne = P.nodes[P.node_off[l] + key];
         ne.zero_base = P.cum[a] - zeros_before;
         ne.one_base = Z + zeros_before;
@@ -196,7 +196,9 @@ static void plan_walk(Plan& P, bool tables) {
   }
 }
 
-static void plan_shape(Plan& P, uint32_t l2_bits) {
+// walk_levels: node levels filled now (the construct path fills level 0 only
+// and the rest while level 0 runs on the device)
+static void plan_shape(Plan& P, uint32_t l2_bits, uint32_t walk_levels = ~0u) {
   (void)l2_bits;
   const uint32_t s = P.sigma, L = P.L;
   P.cum.assign(s + 1, 0);
@@ -222,7 +224,7 @@ static void plan_shape(Plan& P, uint32_t l2_bits) {
   for (uint32_t l = 0; l < L; ++l) P.node_off[l + 1] = P.node_off[l] + (1ull << l);
   P.nodes.swap(node_cache());  // reuse the last build's pages (given back after the upload)
   P.nodes.assign(P.node_off[L], NodeEnt{0, 0, {-1, -1}});
-  plan_walk(P, false);
+  plan_walk(P, false, walk_levels);
   P.code_bytes = L <= 8 ? 1 : 2;
 }
 
@@ -337,7 +339,7 @@ static void fill_treedev(wt_tree* t) {
 // makes while earlier levels run), alloc_query_tables after the last launch
 // (its uploads run on a side stream from pinned staging, overlapping the
 // levels).  alloc_tree does all three synchronously (load / replicate).
-static int alloc_tree_core(wt_tree* t, cudaStream_t st) {
+static int alloc_tree_core(wt_tree* t, cudaStream_t st, uint64_t node_upload = ~0ull) {
   const Plan& P = t->plan;
   t->lv.assign(P.L, LevelHost{});
   for (uint32_t l = 0; l < P.L; ++l) {
@@ -381,9 +383,9 @@ static int alloc_tree_core(wt_tree* t, cudaStream_t st) {
   }
   TRY(dalloc(&t->nodes, P.nodes.size(), st));
   // (pageable source: the call returns once the bytes are staged)
-  if (!P.nodes.empty())
-    CU(cudaMemcpyAsync(t->nodes, P.nodes.data(), P.nodes.size() * sizeof(NodeEnt),
-                       cudaMemcpyHostToDevice, st));
+  const uint64_t nup = std::min<uint64_t>(P.nodes.size(), node_upload);
+  if (nup)
+    CU(cudaMemcpyAsync(t->nodes, P.nodes.data(), nup * sizeof(NodeEnt), cudaMemcpyHostToDevice, st));
   uint64_t bytes = P.n_words * 8 + P.nodes.size() * sizeof(NodeEnt) + P.sigma * 14 + 8;
   for (auto& h : t->lv)
     bytes += h.meta.n_l1 * 8 + h.meta.n_l2 * 2 + 2 * (h.meta.n_bits / t->meta.sample_rate) * 8 +
@@ -719,7 +721,11 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
     tr.mark("alphabet done");
     plan_codes(P);
     tr.mark("codes done");
-    plan_shape(P, l2_bits);
+    // Levels >= 1 of the node table (O(sigma), ~0.6 ms at sigma = 2^16) are
+    // walked on the host while level 0 runs: level 0 reads only the root.
+    // (L <= 2: level 0 is part of the pair pass, which reads level 1 too.)
+    const bool defer_walk = P.L >= 3 && !(getenv("WT_DEFER_WALK") && getenv("WT_DEFER_WALK")[0] == '0');
+    plan_shape(P, l2_bits, defer_walk ? 1u : ~0u);
     tr.mark("plan done");
 
     t->meta.n = n;
@@ -745,7 +751,7 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       else cudaGetLastError();
       tr.mark("pool probe");
     }
-    TRY(alloc_tree_core(t, st));
+    TRY(alloc_tree_core(t, st, defer_walk ? 1ull : ~0ull));
     tr.mark("tree allocated");
     // query tables: uploads on a side stream (pinned staging) once level 0 is
     // queued, so they overlap the levels; `st` joins them at its end
@@ -917,6 +923,15 @@ extern "C" int wt_construct(const void* text, uint64_t n, int sym_bytes, int tex
       };
       int ci = 0;
       for (uint32_t l = 0; l < P.L; ++l) {
+        if (l == 1 && defer_walk) {  // level 0 is queued: the rest of the node table
+          plan_walk(P, false);
+          for (uint32_t k = 0; k < P.L; ++k) t->lv[k].meta.n_nodes = P.n_nodes[k];
+          // (pageable source: staged before the call returns; stream order
+          // puts the copy ahead of level 1)
+          CU(cudaMemcpyAsync(t->nodes, P.nodes.data(), P.nodes.size() * sizeof(NodeEnt),
+                             cudaMemcpyHostToDevice, st));
+          tr.mark("node table walked");
+        }
         if (l == 1 && !tables_done) TRY(query_tables());  // level 0 is queued: overlap it
         const uint64_t m = (uint64_t)P.sizes[l];
         CU(cudaEventRecord(lev[l], st));
